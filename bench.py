@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the MGRIT fine-propagator path (BASELINE.json metric:
+fine space-time point-updates/s of the WENO5 + SSP-RK3 propagator in MGRIT
+relaxation; s/iter).
+
+Workload (BASELINE.json configs[1], "c2"): 1D Burgers, N_x = 512, N_t = 4096,
+CFL 0.4, WENO5-JS (eps 1e-6) + global LF + SSP-RK3, fp64, seeded 4-mode
+Fourier IC (seed 1234), m = 4, FCF relaxation.  One step = one complete FCF
+relaxation of the finest level over all 1024 CF-intervals, F-points written
+to HBM: (2m - 1) * N_t/m * N_x = 3,670,016 point-updates, exactly the
+propagator applications the reference's relax(0) performs (mgrit.py:193-197).
+The input iterate is the serial solution's C-points (finite data); each step
+relaxes the previous step's output.  L2 (126 MB) is flushed between steps
+(outside the timed region).  ``iteration_ms`` additionally times one whole
+V-cycle iteration + residual row of the same config from its initial
+iterate (the reference's MGRIT iteration 1; the config diverges there).
+
+``--impl reference`` times the CPU oracle port (oracle/, a bit-exact C
+restatement of the reference propagator, all host threads) on the same
+relaxation -- the reference itself is Python/NumPy and is not installable
+on the GPU box.
+"""
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import argparse  # noqa: E402
+import ctypes  # noqa: E402
+import json  # noqa: E402
+import math  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "point-updates/s"
+FLOPS_PER_PT = {  # literal FP64 add/sub/mul/div per point-update
+    (2, 3): 735, (2, 2): 489, (1, 3): 297, (1, 2): 197, (0, 3): 45, (0, 2): 29, (0, 1): 13}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def workload(name):
+    import paper_2104_09404_b200 as P
+    pb = P.BASELINE_CONFIGS[name]
+    if name == "c4":  # heaviest C4 case: WENO5 / SSP-RK3, m = 2, FCF
+        pb = pb.scaled(m=2, weno_order=(5,), stepper=("ssprk3",), relaxation="fcf")
+    return pb
+
+
+def relax_units(pb) -> int:
+    return (2 * pb.m - 1) * (pb.n_t // pb.m) * pb.n_x
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm (oracle port)
+# ---------------------------------------------------------------------------
+
+def cpu_relax_setup(pb):
+    import oracle
+    from oracle import mgrit_oracle
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    p = pb.phi_params(0)
+    nthreads = oracle.lib().ora_max_threads()
+    st = oracle.OracleStepper(model=p["model"], k=p["k"], rk_order=p["rk_order"],
+                              dt=p["dt"], dx=p["dx"], eps=p["eps"], speed=p["speed"],
+                              nthreads=nthreads)
+    h = mgrit_oracle.Hierarchy([st] * pb.n_levels, u0, pb.n_t, tg.dt,
+                               mgrit_oracle.Options(n_levels=pb.n_levels, m=pb.m,
+                                                    relaxation="fcf"))
+    # start from the serial trajectory (finite data), as the GPU arm does
+    h.levels[0].u[:] = mgrit_oracle.march(st, u0, pb.n_t)
+    return h, nthreads
+
+
+def cpu_relax_rate(pb, seconds: float):
+    h, nthreads = cpu_relax_setup(pb)
+    units = relax_units(pb)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        h.relax(0)
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return units * done / el, nthreads, done, el
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    pb = workload(args.workload)
+    h, nthreads = cpu_relax_setup(pb)
+    units = relax_units(pb)
+    for _ in range(args.warmup):
+        h.relax(0)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        h.relax(0)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = units * args.steps / total
+    sample = (f"{args.steps} full FCF relaxations of the finest level "
+              f"({units} point-updates each), oracle C port, {nthreads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(pb, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(pb, args):
+    return {"workload": f"{args.workload}: {pb.name}", "n_x": pb.n_x, "n_t": pb.n_t,
+            "m": pb.m, "n_levels": pb.n_levels, "relaxation": "fcf",
+            "scheme": f"WENO{pb.weno_order[0]}+{pb.stepper[0]}+global-LF",
+            "cfl": pb.cfl, "seed": pb.seed,
+            "step": "one FCF relaxation of the finest level, all CF-intervals, "
+                    "F-points stored",
+            "point_updates_per_step": relax_units(pb),
+            "l2": "flushed (256 MiB write) between timed steps"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def fp64_peak():
+    path = os.path.join(ROOT, "tools", "libfp64probe.so")
+    if not os.path.exists(path):
+        return None, None
+    lib = ctypes.CDLL(path)
+    lib.fp64_probe.restype = ctypes.c_double
+    lib.fp64_probe.argtypes = [ctypes.c_int, ctypes.c_int]
+    addmul = lib.fp64_probe(0, 4000)
+    fma = lib.fp64_probe(1, 4000)
+    return (addmul if addmul > 0 else None), (fma if fma > 0 else None)
+
+
+def load_profile_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2104_09404_b200 as P
+    from paper_2104_09404_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pb = workload(args.workload)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    sg = pb.space_grid()
+    steppers = pb.steppers(tg)
+    units = relax_units(pb)
+    k = (pb.weno_order[0] - 1) // 2
+    rk = {"fe": 1, "ssprk2": 2, "ssprk3": 3}[pb.stepper[0]]
+    flops_pt = FLOPS_PER_PT.get((k, rk))
+
+    # finite input iterate: the serial solution's C-points
+    serial = P.serial.march(steppers[0], u0, pb.n_t)
+    h = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+    h._c[h._cur].copy_(serial[::pb.m, 0])
+    h._pristine = False
+    h.f_relax(0)
+    traj = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # kernel-level events: wrap every launch of a step
+    kern_ms = []
+
+    def step(record_kernels=False):
+        if record_kernels:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            e[0].record(stream)
+            h.c_relax(0)          # fused F + C (m steps per chunk)
+            e[1].record(stream)
+            h.f_relax(0)
+            e[2].record(stream)
+            h.fine_values(out=traj)   # F-relax with every F-point stored
+            e[3].record(stream)
+            return e
+        h.relax(0)
+        h.fine_values(out=traj)
+        return None
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    launches0 = _lib.launch_count()
+    clocks = ClockSampler(torch.cuda.current_device()) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    kevents = []
+    for _ in range(args.steps):
+        flush.zero_()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        ev = step(record_kernels=True)
+        s1.record(stream)
+        kevents.append(ev)
+        step_ms.append((s0, s1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop() if clocks else None
+    launches = _lib.launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in step_ms)
+    k_fc = [ev[0].elapsed_time(ev[1]) for ev in kevents]
+    k_f = [ev[2].elapsed_time(ev[3]) for ev in kevents]
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = units * args.steps * world / (total_ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers --------------
+    nc = pb.n_t // pb.m
+    host_in = torch.empty(nc + 1, pb.n_x, dtype=torch.float64).pin_memory()
+    host_in.copy_(serial[::pb.m, 0].cpu())
+    host_out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h.load_c_points(host_in)            # H2D of the step's input iterate
+        h.relax(0)
+        host_out.copy_(h.fine_values(out=traj), non_blocking=True)   # D2H
+        b.record(stream)
+        if i >= args.warmup:
+            e2e_ms.append((a, b))
+    torch.cuda.synchronize()
+    e2e_total = sum(a.elapsed_time(b) for a, b in e2e_ms)
+    e2e_value = units * args.steps / (e2e_total * 1e-3)
+
+    # ---- one whole MGRIT iteration (V-cycle + residual) from the IC --------
+    it_ms = []
+    for i in range(4):
+        hi = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        hi.run_cycle()
+        mon = hi.monitor()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            it_ms.append(a.elapsed_time(b))
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak_addmul, peak_fma = fp64_peak()
+    prof = load_profile_traffic()
+    kernel_ms = sum(k_fc) + sum(k_f)
+    kernel_units = (pb.m * nc * pb.n_x + (pb.m - 1) * nc * pb.n_x) * args.steps
+    achieved = flops_pt * kernel_units / (kernel_ms * 1e-3) / 1e12 if flops_pt else None
+    roofline = {
+        "bound": "fp64",
+        "kernel": f"sweep_kernel<{k},burgers> (fused F/C relaxation)",
+        "achieved": achieved, "unit": "TFLOP/s",
+        "peak": peak_addmul / 1e12 if peak_addmul else None,
+        "peak_source": "measured: tools/fp64_peak.cu DADD/DMUL issue rate, 1 op = 1 flop "
+                       "(MEASURED_PEAKS.json has no FP64 figure)",
+        "frac": (achieved / (peak_addmul / 1e12)) if (achieved and peak_addmul) else None,
+        "peak_fma": 2 * peak_fma / 1e12 if peak_fma else None,
+        "frac_of_fma_peak": (achieved / (2 * peak_fma / 1e12)) if (achieved and peak_fma) else None,
+        "flops_per_point_update": flops_pt,
+        "kernel_share_of_step": kernel_ms / (total_ms * args.steps / args.steps)
+        if total_ms else None,
+        "traffic": prof.get("dram_bytes_per_launch"),
+        "algorithmic_bytes_per_launch": 16 * pb.m * nc * pb.n_x,
+    }
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(pb, args),
+        "roofline": roofline,
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": host_in.numel() * 8,
+                "d2h_bytes_per_step": host_out.numel() * 8},
+        "gpu_launches": launches,
+        "clocks": clock_info,
+        "iteration_ms": statistics.median(it_ms),
+        "iteration_note": "one V-cycle (FCF, 2 levels, 1024-step sequential coarse solve) "
+                          "+ residual row from the initial iterate; config diverges in it. 1 "
+                          f"(residual after: {mon.residual})",
+        "kernel_ms": {"fused_f_c": statistics.median(k_fc), "f_store": statistics.median(k_f)},
+    }
+    if not args.no_cpu_baseline and world == 1:
+        rate, cores, n, el = cpu_relax_rate(pb, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": f"{n} full FCF relaxation(s) of the same workload "
+                                          f"in {el:.1f} s (oracle C port)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

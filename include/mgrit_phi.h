@@ -1,0 +1,165 @@
+/*
+ * mgrit_phi.h -- C ABI of the B200 MGRIT fine-propagator library
+ * (paper_2104_09404_b200/libmgrit_phi.so).
+ *
+ * The reference (arxiv 2104.09404, package `mgritlab`) is pure Python/NumPy;
+ * its "FFI" for this path is Python calling the functions below through
+ * ctypes.  Each entry point replaces one reference
+ * interface, cited as pkg/src/mgritlab/<file>:<lines>:
+ *
+ *   mgp_sweep        -- the batched propagator and every level operation
+ *                       built from it:
+ *                         RungeKuttaStepper.advance   stepper.py:50-82
+ *                         SemiDiscreteOperator.rhs    flux.py:129-161
+ *                         MgritHierarchy.f_relax      mgrit.py:168-180
+ *                         MgritHierarchy.c_relax      mgrit.py:182-191
+ *                         MgritHierarchy.restrict     mgrit.py:199-217
+ *                         MgritHierarchy.coarse_solve mgrit.py:219-226
+ *                         MgritHierarchy.residual_norm mgrit.py:264-270
+ *                         rel_l2_spacetime_error      grid.py:96-108
+ *                         solve_serial                serial.py:40-61
+ *   mgp_sum_partials -- deterministic reduction of the per-chunk partial sums
+ *                       the sweep writes (residual^2, error^2, non-finite
+ *                       count), replacing np.linalg.norm (mgrit.py:270,
+ *                       grid.py:105-108) and np.isfinite (mgrit.py:323).
+ *
+ * Conventions: all pointers are device pointers owned by the caller; states
+ * are rows of `nx` float64 cells; strides are in elements (float64), may be
+ * 0 to broadcast one row.  Every call is asynchronous on `stream`
+ * (a cudaStream_t, NULL = legacy default stream).  Return codes: MGP_OK,
+ * MGP_EINVAL (bad argument: the Python layer raises ConfigError, mirroring
+ * the reference's constructor checks), MGP_ECUDA (launch/CUDA failure:
+ * RuntimeError).  Non-finite data never fails a call: NaN/inf propagate like
+ * NumPy.  The library owns no device memory.
+ */
+#ifndef MGRIT_PHI_H
+#define MGRIT_PHI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGP_OK 0
+#define MGP_EINVAL 1
+#define MGP_ECUDA 2
+
+/* models.py:101-133 (Burgers) and the linear-advection model BASELINE.json
+ * config 1 needs (flux a*u, |lambda| = |a|). */
+#define MGP_MODEL_BURGERS 0
+#define MGP_MODEL_ADVECTION 1
+
+/* NumPy candidate-sum order of weno.py:175:
+ * SEQ when advance() received >= 2 fields, LANE2 for a single field. */
+#define MGP_SUM_SEQ 0
+#define MGP_SUM_LANE2 1
+
+/* how "+ g" is applied after a propagator application */
+#define MGP_G_NONE 0   /* no addition (advance, serial march)              */
+#define MGP_G_ZERO 1   /* + 0.0 (finest-level g, zero past node 0)         */
+#define MGP_G_ARRAY 2  /* + g[row]                                         */
+
+/* what the sweep does after its chained steps */
+#define MGP_TAIL_NONE 0
+#define MGP_TAIL_PHI 1       /* tail_out = Phi(x) (+ g_tail per tail_g_mode)  */
+#define MGP_TAIL_RESTRICT 2  /* FAS restriction, mgrit.py:209-215 (below)    */
+#define MGP_TAIL_RESID 3     /* residual (g + Phi(x)) - target, mgrit.py:268 */
+
+#define MGP_GUESS_LAST_STEP 0
+#define MGP_GUESS_INJECTION 1
+
+/* One propagator Phi_l: SSP-RK(rk_order) over the WENO(2k+1)/global-LF
+ * semi-discrete operator on a periodic mesh of nx cells
+ * (harness.py:350-355 builds one per level with dt = dt0 * m**l). */
+typedef struct mgp_phi {
+    int32_t model;      /* MGP_MODEL_*                                        */
+    int32_t weno_k;     /* reconstruction degree 0..3 (order 2k+1), flux.py:35 */
+    int32_t rk_order;   /* 1 FE, 2 SSP-RK2, 3 SSP-RK3; 0 = semi-discrete rhs */
+    int32_t regime;     /* MGP_SUM_* for chained steps                        */
+    int64_t nx;         /* cells, >= 2k+1 (flux.py:138-141)                   */
+    double dt;          /* step size of this level                             */
+    double dx;          /* SpatialGrid.dx = length / nx (grid.py:35-37)        */
+    double epsilon;     /* WENO epsilon > 0 (weno.py:30)                       */
+    double speed;       /* advection speed a (ignored for Burgers)             */
+} mgp_phi;
+
+/*
+ * mgp_sweep: for every chunk b in [0, n_chunks), independently:
+ *
+ *   x = start[b*start_stride]                                   (row)
+ *   [err/nonfinite accounting of x against ref[b*ref_cs]]
+ *   for s = 1 .. n_steps:                                      (chained steps)
+ *       x = Phi(x) (+ g[b*g_cs + (s-1)*g_ss] per g_mode)
+ *       if store: store[b*st_cs + (s-1)*st_ss] = x
+ *       [err/nonfinite accounting of x against ref[b*ref_cs + s*ref_ss]]
+ *   tail (with the tail regime `tail_regime`):
+ *     MGP_TAIL_PHI:      y = Phi(x) (+ tail_g[b*tg_s] per tail_g_mode);
+ *                        tail_out[b*to_s] = y
+ *     MGP_TAIL_RESTRICT: psi = Phi(x);  gf = tail_g row (tail_g_mode),
+ *                        phi = aux[b*aux_s];
+ *                        tail_out[b*to_s]  = (gf + phi) - psi      (coarse g)
+ *                        tail_out2[b*to2_s] = guess == LAST_STEP
+ *                                             ? phi + gf : aux2[b*aux2_s]
+ *     MGP_TAIL_RESID:    r = (gf + Phi(x)) - aux[b*aux_s];
+ *                        partials[3b+0] = sum over cells of r*r
+ *                        (last chunk also accounts aux row in err/nonfinite
+ *                         against ref[(b+1)*ref_cs] when ref_last_next != 0)
+ *   partials (if non-NULL): [3b+0] residual^2, [3b+1] error^2 (ref non-NULL),
+ *   [3b+2] number of non-finite cells seen (when count_nonfinite != 0).
+ *
+ * n_chunks = 1 with store of every step is the sequential coarse solve /
+ * serial march.  Chunks never read rows another chunk writes in the same
+ * call (the caller guarantees it, e.g. by writing new C-points to a
+ * separate buffer), so all chunks run concurrently.
+ */
+typedef struct mgp_sweep_args {
+    mgp_phi phi;
+    int64_t n_chunks;
+    const double *start;  int64_t start_stride;
+    int32_t n_steps;      int32_t g_mode;
+    const double *g;      int64_t g_cs, g_ss;
+    double *store;        int64_t st_cs, st_ss;
+    int32_t tail;         int32_t tail_regime;
+    int32_t tail_g_mode;  int32_t guess;
+    const double *tail_g; int64_t tg_s;
+    double *tail_out;     int64_t to_s;
+    double *tail_out2;    int64_t to2_s;
+    const double *aux;    int64_t aux_s;
+    const double *aux2;   int64_t aux2_s;
+    const double *ref;    int64_t ref_cs, ref_ss;
+    int32_t ref_last_next;
+    int32_t count_nonfinite;
+    double *partials;
+} mgp_sweep_args;
+
+int mgp_sweep(const mgp_sweep_args *args, void *stream);
+
+/* out[j] = sum_b partials[width*b + j] for j < width (width <= 4), summed in a
+ * fixed order independent of launch timing (deterministic). */
+int mgp_sum_partials(const double *partials, int64_t n, int32_t width,
+                     double *out, void *stream);
+
+/* Largest nx a single fused field CTA handles (whole field in shared memory). */
+int64_t mgp_max_nx(void);
+
+/* Library/ABI version and the compile-time WENO tables of degree k, written
+ * as cw[4][4], d[4], sm[4][4][4] (row-major, zero padded) so tests can check
+ * them against float(Fraction(p, q)) of weno.py:43-86. */
+int32_t mgp_abi_version(void);
+int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64);
+
+/* Number of kernel launches issued by this library since load (for the
+ * bench's gpu_launches accounting). */
+int64_t mgp_launch_count(void);
+
+/* ABI self-description for binding checks: writes sizeof(mgp_phi),
+ * sizeof(mgp_sweep_args) and then offsetof() of every mgp_sweep_args field
+ * in declaration order to out[0..n); returns the number of entries written. */
+int32_t mgp_sweep_args_layout(int64_t *out, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGRIT_PHI_H */

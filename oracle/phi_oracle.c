@@ -1,0 +1,354 @@
+/*
+ * phi_oracle.c -- CPU restatement of the reference fine propagator Phi.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker for the CUDA
+ * path and the "port" CPU baseline timed by `bench.py --impl reference`.  It
+ * is never linked into, loaded by, or called from the product library
+ * paper_2104_09404_b200/libmgrit_phi.so.
+ *
+ * It restates, operation by operation, what the reference computes with
+ * NumPy for RungeKuttaStepper.advance (stepper.py:50-82) over
+ * SemiDiscreteOperator.rhs (flux.py:129-161):
+ *   - periodic windows (weno.py:191-199, 219-221): left window of interface
+ *     i+1/2 = cells i-k..i+k, right window = cells i+1+k, ..., i+1-k, both
+ *     through reconstruct_left (weno.py:234-235);
+ *   - candidates  q_r = sum_t cw[r,t] w_t                      (weno.py:175)
+ *       summed sequentially when advance() got >= 2 fields, and in "2-lane"
+ *       order (even window slots) + (odd window slots) for a single field --
+ *       the NumPy einsum contiguity quirk;
+ *   - smoothness  beta_r = sum_a sum_b (w_a B[r,a,b]) w_b, a-major, from +0
+ *                                                         (weno.py:154-158);
+ *   - weights     raw_r = d_r/((eps+beta_r)(eps+beta_r)), S = sum_r raw_r,
+ *                 omega_r = raw_r/S, value = sum_r omega_r q_r
+ *                                                 (weno.py:161-168,176-177);
+ *   - global LF:  alpha = NaN-propagating max over |uL|, |uR| of the field
+ *                 (flux.py:70-79, models.py:115-117), advection: |a|;
+ *                 F = (0.5 (f(uL)+f(uR))) - ((0.5 alpha)(uR-uL))
+ *                 with f(u) = (0.5 u) u (models.py:107-109)  (flux.py:82-88);
+ *   - rhs         A_i = (-(F_i - F_{i-1})) / dx               (flux.py:159-161);
+ *   - SSP RK 1/2/3 in Shu-Osher form with Python's left-to-right evaluation
+ *     (scalar products such as 0.25*dt first)                (stepper.py:50-62).
+ * Zero table entries are skipped; for finite windows this is exact (0*w is a
+ * signed zero), and a window holding any non-finite value reconstructs to
+ * NaN, which is what the reference's 0*inf terms produce.
+ *
+ * Build: oracle/Makefile (gcc -O3 -ffp-contract=off, no fast-math).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+#include <unistd.h>
+
+#define ORA_MODEL_BURGERS 0
+#define ORA_MODEL_ADVECTION 1
+#define ORA_SUM_SEQ 0
+#define ORA_SUM_LANE2 1
+
+typedef struct {
+    int32_t model;     /* 0 burgers, 1 linear advection                     */
+    int32_t k;         /* WENO degree 0..3 (order 2k+1)                      */
+    int32_t rk_order;  /* 1 FE, 2 SSP-RK2, 3 SSP-RK3; 0 = semi-discrete rhs  */
+    int32_t regime;    /* ORA_SUM_SEQ / ORA_SUM_LANE2                        */
+    double dt, dx, eps, speed;
+} ora_params;
+
+/* ---- exact rational tables, weno.py:43-86.  IEEE division of the small
+ * integers gives the correctly rounded double, i.e. float(Fraction(p, q)). */
+static const int CW_NUM[4][4][4] = {
+    {{1}},
+    {{1, 1}, {-1, 3}},
+    {{2, 5, -1}, {-1, 5, 2}, {2, -7, 11}},
+    {{3, 13, -5, 1}, {-1, 7, 7, -1}, {1, -5, 13, 3}, {-3, 13, -23, 25}}};
+static const int CW_DEN[4] = {1, 2, 6, 12};
+static const int D_NUM[4][4] = {{1}, {2, 1}, {3, 6, 1}, {4, 18, 12, 1}};
+static const int D_DEN[4] = {1, 3, 10, 35};
+static const int SM_NUM[4][4][4][4] = {
+    {{{0}}},
+    {{{1, -1}, {-1, 1}}, {{1, -1}, {-1, 1}}},
+    {{{20, -31, 11}, {-31, 50, -19}, {11, -19, 8}},
+     {{8, -13, 5}, {-13, 26, -13}, {5, -13, 8}},
+     {{8, -19, 11}, {-19, 50, -31}, {11, -31, 20}}},
+    {{{2107, -4701, 3521, -927}, {-4701, 11003, -8623, 2321},
+      {3521, -8623, 7043, -1941}, {-927, 2321, -1941, 547}},
+     {{547, -1261, 961, -247}, {-1261, 3443, -2983, 801},
+      {961, -2983, 2843, -821}, {-247, 801, -821, 267}},
+     {{267, -821, 801, -247}, {-821, 2843, -2983, 961},
+      {801, -2983, 3443, -1261}, {-247, 961, -1261, 547}},
+     {{547, -1941, 2321, -927}, {-1941, 7043, -8623, 3521},
+      {2321, -8623, 11003, -4701}, {-927, 3521, -4701, 2107}}}};
+static const int SM_DEN[4] = {1, 1, 6, 240};
+
+typedef struct {
+    int k;
+    double eps;
+    double cw[4][4];      /* cw[r][j] multiplies window slot (k-r)+j        */
+    double d[4];
+    double sm[4][4][4];   /* sm[r][i][j] pairs window slots (k-r)+i, (k-r)+j */
+} ora_tables;
+
+static void build_tables(int k, double eps, ora_tables *t) {
+    memset(t, 0, sizeof(*t));
+    t->k = k;
+    t->eps = eps;
+    for (int r = 0; r <= k; ++r) {
+        t->d[r] = (double)D_NUM[k][r] / (double)D_DEN[k];
+        for (int j = 0; j <= k; ++j) {
+            t->cw[r][j] = (double)CW_NUM[k][r][j] / (double)CW_DEN[k];
+            for (int i = 0; i <= k; ++i)
+                t->sm[r][i][j] = (double)SM_NUM[k][r][i][j] / (double)SM_DEN[k];
+        }
+    }
+}
+
+/* Exported for the table-equality test (tables vs float(Fraction)). */
+int ora_get_tables(int k, double *cw16, double *d4, double *sm64) {
+    if (k < 0 || k > 3) return 1;
+    ora_tables t;
+    build_tables(k, 1e-6, &t);
+    memcpy(cw16, t.cw, sizeof(t.cw));
+    memcpy(d4, t.d, sizeof(t.d));
+    memcpy(sm64, t.sm, sizeof(t.sm));
+    return 0;
+}
+
+/* reconstruct_left (weno.py:171-177) on the window w[0..2k] */
+static double recon(const ora_tables *t, int regime, const double *w) {
+    const int k = t->k;
+    for (int s = 0; s <= 2 * k; ++s)
+        if (!isfinite(w[s])) return NAN;
+    double q[4] = {0, 0, 0, 0}, raw[4] = {0, 0, 0, 0};
+    for (int r = 0; r <= k; ++r) {
+        const int lo = k - r;
+        if (regime == ORA_SUM_SEQ) {
+            double acc = t->cw[r][0] * w[lo];
+            for (int j = 1; j <= k; ++j) acc = acc + t->cw[r][j] * w[lo + j];
+            q[r] = acc;
+        } else {
+            double ev = 0.0, od = 0.0;
+            int he = 0, ho = 0;
+            for (int j = 0; j <= k; ++j) {
+                const int s = lo + j;
+                const double p = t->cw[r][j] * w[s];
+                if ((s & 1) == 0) { ev = he ? ev + p : p; he = 1; }
+                else { od = ho ? od + p : p; ho = 1; }
+            }
+            q[r] = he ? (ho ? ev + od : ev) : od;
+        }
+        double b = 0.0;
+        for (int i = 0; i <= k; ++i)
+            for (int j = 0; j <= k; ++j)
+                b = b + (w[lo + i] * t->sm[r][i][j]) * w[lo + j];
+        const double e = t->eps + b;
+        raw[r] = t->d[r] / (e * e);
+    }
+    double S = raw[0];
+    for (int r = 1; r <= k; ++r) S = S + raw[r];
+    double v = (raw[0] / S) * q[0];
+    for (int r = 1; r <= k; ++r) v = v + (raw[r] / S) * q[r];
+    return v;
+}
+
+typedef struct {
+    int64_t nx;
+    double *pad;   /* field with k+1 periodic halo cells on both sides */
+    double *ul, *ur, *F, *A, *u1, *u2;
+} ora_work;
+
+static int work_alloc(ora_work *w, int64_t nx, int k) {
+    w->nx = nx;
+    const int64_t H = k + 1;
+    w->pad = (double *)malloc(sizeof(double) * (size_t)(nx + 2 * H));
+    w->ul = (double *)malloc(sizeof(double) * (size_t)nx * 6);
+    if (!w->pad || !w->ul) { free(w->pad); free(w->ul); return 1; }
+    w->ur = w->ul + nx;
+    w->F = w->ur + nx;
+    w->A = w->F + nx;
+    w->u1 = w->A + nx;
+    w->u2 = w->u1 + nx;
+    return 0;
+}
+
+static void work_free(ora_work *w) { free(w->pad); free(w->ul); }
+
+/* SemiDiscreteOperator.rhs (flux.py:159-161) for one field v -> A */
+static void rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
+                      const double *v, double *A) {
+    const int64_t nx = wk->nx;
+    const int k = t->k, H = k + 1;
+    double *pad = wk->pad;
+    for (int64_t i = 0; i < nx; ++i) pad[H + i] = v[i];
+    for (int h = 0; h < H; ++h) {
+        pad[h] = v[((nx - H + h) % nx + nx) % nx];
+        pad[H + nx + h] = v[h % nx];
+    }
+
+    double w[7];
+    for (int64_t i = 0; i < nx; ++i) {
+        const double *c = pad + H + i;              /* cell i */
+        for (int s = 0; s <= 2 * k; ++s) w[s] = c[s - k];
+        wk->ul[i] = recon(t, p->regime, w);
+        for (int s = 0; s <= 2 * k; ++s) w[s] = c[1 + k - s];
+        wk->ur[i] = recon(t, p->regime, w);
+    }
+    double alpha;
+    if (p->model == ORA_MODEL_BURGERS) {
+        /* np.max over interfaces (NaN-propagating), then np.maximum */
+        double ml = 0.0, mr = 0.0;
+        int nan = 0;
+        for (int64_t i = 0; i < nx; ++i) {
+            const double a = fabs(wk->ul[i]), b = fabs(wk->ur[i]);
+            if (isnan(a) || isnan(b)) nan = 1;
+            if (a > ml) ml = a;
+            if (b > mr) mr = b;
+        }
+        alpha = nan ? NAN : (ml > mr ? ml : mr);
+    } else {
+        alpha = fabs(p->speed);
+    }
+    const double half_alpha = 0.5 * alpha;
+    for (int64_t i = 0; i < nx; ++i) {
+        const double l = wk->ul[i], r = wk->ur[i];
+        double fl, fr;
+        if (p->model == ORA_MODEL_BURGERS) { fl = (0.5 * l) * l; fr = (0.5 * r) * r; }
+        else { fl = p->speed * l; fr = p->speed * r; }
+        wk->F[i] = (0.5 * (fl + fr)) - (half_alpha * (r - l));
+    }
+    for (int64_t i = 0; i < nx; ++i) {
+        const double fm = wk->F[i == 0 ? nx - 1 : i - 1];
+        A[i] = (-(wk->F[i] - fm)) / p->dx;
+    }
+}
+
+/* RungeKuttaStepper.advance (stepper.py:50-82) + optional relaxation "+ g" */
+static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
+                      const double *u, const double *g, double *out) {
+    const int64_t nx = wk->nx;
+    double *A = wk->A, *u1 = wk->u1, *u2 = wk->u2;
+    if (p->rk_order == 0) {
+        rhs_field(p, t, wk, u, out);
+        return;
+    }
+    const double dt = p->dt;
+    rhs_field(p, t, wk, u, A);
+    for (int64_t i = 0; i < nx; ++i) u1[i] = u[i] + dt * A[i];
+    if (p->rk_order == 1) {
+        for (int64_t i = 0; i < nx; ++i) out[i] = u1[i];
+    } else if (p->rk_order == 2) {
+        const double hdt = 0.5 * dt;
+        rhs_field(p, t, wk, u1, A);
+        for (int64_t i = 0; i < nx; ++i)
+            out[i] = ((0.5 * u[i]) + (0.5 * u1[i])) + (hdt * A[i]);
+    } else {
+        const double qdt = 0.25 * dt;
+        const double two3 = 2.0 / 3.0;
+        const double tdt = two3 * dt;
+        rhs_field(p, t, wk, u1, A);
+        for (int64_t i = 0; i < nx; ++i)
+            u2[i] = ((0.75 * u[i]) + (0.25 * u1[i])) + (qdt * A[i]);
+        rhs_field(p, t, wk, u2, A);
+        for (int64_t i = 0; i < nx; ++i)
+            out[i] = ((u[i] / 3.0) + (two3 * u2[i])) + (tdt * A[i]);
+    }
+    if (g)
+        for (int64_t i = 0; i < nx; ++i) out[i] = out[i] + g[i];
+}
+
+static int check_params(const ora_params *p, int64_t nx) {
+    if (!p || p->k < 0 || p->k > 3) return 1;
+    if (p->rk_order < 0 || p->rk_order > 3) return 1;
+    if (p->model != ORA_MODEL_BURGERS && p->model != ORA_MODEL_ADVECTION) return 1;
+    if (p->regime != ORA_SUM_SEQ && p->regime != ORA_SUM_LANE2) return 1;
+    if (nx < 2 * p->k + 1) return 1;
+    return 0;
+}
+
+/* worker pool: fields are independent, threads take them off a shared counter */
+typedef struct {
+    const ora_params *p;
+    const ora_tables *t;
+    const double *u, *g;
+    double *out;
+    int64_t u_stride, g_stride, out_stride, batch, nx;
+    int64_t next;
+    pthread_mutex_t lock;
+    int err;
+} ora_job;
+
+static void *ora_worker(void *arg) {
+    ora_job *job = (ora_job *)arg;
+    ora_work wk;
+    if (work_alloc(&wk, job->nx, job->p->k)) {
+        pthread_mutex_lock(&job->lock);
+        job->err = 1;
+        pthread_mutex_unlock(&job->lock);
+        return NULL;
+    }
+    for (;;) {
+        pthread_mutex_lock(&job->lock);
+        const int64_t b = job->next++;
+        pthread_mutex_unlock(&job->lock);
+        if (b >= job->batch) break;
+        phi_field(job->p, job->t, &wk, job->u + b * job->u_stride,
+                  job->g ? job->g + b * job->g_stride : NULL,
+                  job->out + b * job->out_stride);
+    }
+    work_free(&wk);
+    return NULL;
+}
+
+int ora_max_threads(void) {
+    long n = sysconf(_SC_NPROCESSORS_ONLN);
+    return n > 0 ? (int)n : 1;
+}
+
+/*
+ * out[b] = Phi(u[b]) (+ g[b] when g != NULL) for b < batch; rows of nx
+ * doubles with the given strides (in elements).  u_stride 0 broadcasts one
+ * state.  Fields are independent and are spread over nthreads POSIX threads
+ * (nthreads <= 0: one per online core).  Returns 0, 1 on bad arguments, 2 on
+ * allocation failure.
+ */
+int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
+                  const double *g, int64_t g_stride, double *out,
+                  int64_t out_stride, int64_t batch, int64_t nx, int nthreads) {
+    if (check_params(p, nx) || batch < 0) return 1;
+    ora_tables t;
+    build_tables(p->k, p->eps, &t);
+    if (nthreads <= 0) nthreads = ora_max_threads();
+    if (nthreads > batch) nthreads = batch > 0 ? (int)batch : 1;
+    ora_job job = {p, &t, u, g, out, u_stride, g_stride, out_stride, batch, nx,
+                   0, PTHREAD_MUTEX_INITIALIZER, 0};
+    if (nthreads == 1) {
+        ora_worker(&job);
+        return job.err ? 2 : 0;
+    }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    if (!th) return 2;
+    int started = 0;
+    for (int i = 0; i < nthreads; ++i)
+        if (pthread_create(&th[i], NULL, ora_worker, &job) == 0) ++started;
+    if (started == 0) ora_worker(&job);
+    for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
+    free(th);
+    return job.err ? 2 : 0;
+}
+
+/*
+ * Sequential marching (MgritHierarchy.coarse_solve, mgrit.py:219-226, and
+ * solve_serial, serial.py:40-61): u[i] = Phi(u[i-1]) (+ g[i]) for
+ * i = 1..n_steps; u and g hold n_steps+1 rows of nx doubles.
+ */
+int ora_march(const ora_params *p, double *u, const double *g, int64_t n_steps,
+              int64_t nx) {
+    if (check_params(p, nx) || n_steps < 0) return 1;
+    ora_tables t;
+    build_tables(p->k, p->eps, &t);
+    ora_work wk;
+    if (work_alloc(&wk, nx, p->k)) return 2;
+    for (int64_t i = 1; i <= n_steps; ++i)
+        phi_field(p, &t, &wk, u + (i - 1) * nx, g ? g + i * nx : NULL, u + i * nx);
+    work_free(&wk);
+    return 0;
+}

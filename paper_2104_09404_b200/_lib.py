@@ -1,0 +1,133 @@
+"""ctypes binding of the C ABI in ``include/mgrit_phi.h``.
+
+The reference is Python; its foreign-function boundary for this path is
+Python calling the shared library through ctypes, exactly as this module
+does.  PyTorch supplies device memory and the current CUDA stream (plumbing);
+all arithmetic of the path runs in ``libmgrit_phi.so``.  There is no CPU
+fallback: if the library or a CUDA device is missing, every entry point
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+from .errors import ConfigError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libmgrit_phi.so")
+SRC_PATH = os.path.join(_PKG, "csrc", "mgrit_phi.cu")
+HEADER_PATH = os.path.join(_ROOT, "include", "mgrit_phi.h")
+
+MGP_OK, MGP_EINVAL, MGP_ECUDA = 0, 1, 2
+SUM_SEQ, SUM_LANE2 = 0, 1
+G_NONE, G_ZERO, G_ARRAY = 0, 1, 2
+TAIL_NONE, TAIL_PHI, TAIL_RESTRICT, TAIL_RESID = 0, 1, 2, 3
+GUESS_LAST_STEP, GUESS_INJECTION = 0, 1
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    # bit parity with NumPy: no FMA contraction, IEEE division and sqrt
+    "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
+    "-diag-suppress", "128",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+class MgpPhi(ctypes.Structure):
+    _fields_ = [("model", ctypes.c_int32), ("weno_k", ctypes.c_int32),
+                ("rk_order", ctypes.c_int32), ("regime", ctypes.c_int32),
+                ("nx", ctypes.c_int64), ("dt", ctypes.c_double),
+                ("dx", ctypes.c_double), ("epsilon", ctypes.c_double),
+                ("speed", ctypes.c_double)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+
+
+class MgpSweepArgs(ctypes.Structure):
+    _fields_ = [
+        ("phi", MgpPhi),
+        ("n_chunks", _I64),
+        ("start", _P), ("start_stride", _I64),
+        ("n_steps", _I32), ("g_mode", _I32),
+        ("g", _P), ("g_cs", _I64), ("g_ss", _I64),
+        ("store", _P), ("st_cs", _I64), ("st_ss", _I64),
+        ("tail", _I32), ("tail_regime", _I32),
+        ("tail_g_mode", _I32), ("guess", _I32),
+        ("tail_g", _P), ("tg_s", _I64),
+        ("tail_out", _P), ("to_s", _I64),
+        ("tail_out2", _P), ("to2_s", _I64),
+        ("aux", _P), ("aux_s", _I64),
+        ("aux2", _P), ("aux2_s", _I64),
+        ("ref", _P), ("ref_cs", _I64), ("ref_ss", _I64),
+        ("ref_last_next", _I32),
+        ("count_nonfinite", _I32),
+        ("partials", _P),
+    ]
+
+
+EXPORTED_SYMBOLS = ("mgp_sweep", "mgp_sum_partials", "mgp_max_nx",
+                    "mgp_abi_version", "mgp_weno_tables", "mgp_launch_count",
+                    "mgp_sweep_args_layout")
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libmgrit_phi.so for sm_100a with nvcc (no GPU needed)."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"),
+           "-o", LIB_PATH, SRC_PATH]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def load():
+    """Load the library (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    lib.mgp_sweep.argtypes = [ctypes.POINTER(MgpSweepArgs), _P]
+    lib.mgp_sweep.restype = ctypes.c_int
+    lib.mgp_sum_partials.argtypes = [_P, _I64, _I32, _P, _P]
+    lib.mgp_sum_partials.restype = ctypes.c_int
+    lib.mgp_max_nx.restype = _I64
+    lib.mgp_abi_version.restype = _I32
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib.mgp_weno_tables.argtypes = [_I32, dp, dp, dp]
+    lib.mgp_weno_tables.restype = ctypes.c_int
+    lib.mgp_launch_count.restype = _I64
+    lib.mgp_sweep_args_layout.argtypes = [ctypes.POINTER(_I64), _I32]
+    lib.mgp_sweep_args_layout.restype = _I32
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == MGP_OK:
+        return
+    if rc == MGP_EINVAL:
+        raise ConfigError(f"{what}: invalid argument for the B200 kernels")
+    raise RuntimeError(f"{what}: CUDA failure (status {rc})")
+
+
+def launch_count() -> int:
+    return int(load().mgp_launch_count())
+
+
+def max_nx() -> int:
+    return int(load().mgp_max_nx())

@@ -1,0 +1,89 @@
+"""Device plumbing: torch tensors in, ``mgp_sweep`` launches out.
+
+Every launch goes through :func:`sweep`, the single Python-side caller of
+the C entry point ``mgp_sweep`` (include/mgrit_phi.h).  Tensors are float64
+CUDA tensors; row pointers are passed as raw addresses with element strides.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (G_NONE, MgpPhi, MgpSweepArgs, SUM_LANE2, SUM_SEQ,
+                   TAIL_NONE)
+
+DTYPE = torch.float64
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 MGRIT path needs a CUDA device "
+                           "(there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def to_device(u) -> torch.Tensor:
+    """float64, contiguous, on the current CUDA device."""
+    if torch.is_tensor(u):
+        t = u.to(device=device(), dtype=DTYPE)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(u, dtype=np.float64)).to(device())
+    return t.contiguous()
+
+
+def regime_for_batch(n_fields: int) -> int:
+    """NumPy's candidate-sum order in the reference for an advance() call on
+    n_fields fields (checked by the golden tests)."""
+    return SUM_SEQ if n_fields >= 2 else SUM_LANE2
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
+          n_steps: int = 0, g_mode: int = G_NONE, g=None, g_cs: int = 0,
+          g_ss: int = 0, store=None, st_cs: int = 0, st_ss: int = 0,
+          tail: int = TAIL_NONE, tail_regime: int = SUM_SEQ,
+          tail_g_mode: int = G_NONE, guess: int = 0, tail_g=None,
+          tg_s: int = 0, tail_out=None, to_s: int = 0, tail_out2=None,
+          to2_s: int = 0, aux=None, aux_s: int = 0, aux2=None, aux2_s: int = 0,
+          ref=None, ref_cs: int = 0, ref_ss: int = 0, ref_last_next: int = 0,
+          count_nonfinite: int = 0, partials=None, what: str = "mgp_sweep"):
+    a = MgpSweepArgs()
+    a.phi = phi
+    a.n_chunks = int(n_chunks)
+    a.start, a.start_stride = ptr(start), int(start_stride)
+    a.n_steps, a.g_mode = int(n_steps), int(g_mode)
+    a.g, a.g_cs, a.g_ss = ptr(g), int(g_cs), int(g_ss)
+    a.store, a.st_cs, a.st_ss = ptr(store), int(st_cs), int(st_ss)
+    a.tail, a.tail_regime = int(tail), int(tail_regime)
+    a.tail_g_mode, a.guess = int(tail_g_mode), int(guess)
+    a.tail_g, a.tg_s = ptr(tail_g), int(tg_s)
+    a.tail_out, a.to_s = ptr(tail_out), int(to_s)
+    a.tail_out2, a.to2_s = ptr(tail_out2), int(to2_s)
+    a.aux, a.aux_s = ptr(aux), int(aux_s)
+    a.aux2, a.aux2_s = ptr(aux2), int(aux2_s)
+    a.ref, a.ref_cs, a.ref_ss = ptr(ref), int(ref_cs), int(ref_ss)
+    a.ref_last_next = int(ref_last_next)
+    a.count_nonfinite = int(count_nonfinite)
+    a.partials = ptr(partials)
+    rc = _lib.load().mgp_sweep(ctypes.byref(a), ctypes.c_void_p(stream_handle()))
+    _lib.check(rc, what)
+
+
+def sum_partials(partials: torch.Tensor, n: int, width: int, out: torch.Tensor):
+    rc = _lib.load().mgp_sum_partials(ptr(partials), int(n), int(width), ptr(out),
+                                      ctypes.c_void_p(stream_handle()))
+    _lib.check(rc, "mgp_sum_partials")

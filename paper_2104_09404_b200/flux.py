@@ -1,0 +1,113 @@
+"""Semi-discrete finite-volume operator (WENO + global Lax-Friedrichs).
+
+Mirrors reference ``pkg/src/mgritlab/flux.py``: ``WenoConfig`` /
+``FluxConfig`` validation (flux.py:35-67), ``SemiDiscreteOperator``
+constructor checks (:129-145) and ``rhs`` (:159-161).  The operator only
+holds parameters; ``rhs(field)`` runs on the GPU (``mgp_sweep`` with
+rk_order 0).  The Roe flux (flux.py:91-126) is outside the GPU path's scope
+and is rejected with ConfigError, as are systems; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import device as dev
+from ._lib import MgpPhi, TAIL_PHI
+from .errors import ConfigError, DimensionError
+from .grid import SpatialGrid
+from .models import ConservationModel
+from .weno import DEFAULT_EPSILON, SUPPORTED_DEGREES, build_tables
+
+FLUX_KINDS = ("lf", "roe")
+
+
+@dataclass(frozen=True)
+class WenoConfig:
+    """Reconstruction settings: nominal order s = 2k+1 (flux.py:35-54)."""
+
+    order: int = 1
+    epsilon: float = DEFAULT_EPSILON
+    characteristic: bool = True  # no effect for scalar models (weno.py:222)
+
+    def __post_init__(self):
+        if self.order % 2 == 0 or self.degree not in SUPPORTED_DEGREES:
+            supported = tuple(2 * k + 1 for k in SUPPORTED_DEGREES)
+            raise ConfigError(f"unsupported reconstruction order {self.order}, "
+                              f"expected one of {supported}")
+        if self.epsilon <= 0.0:
+            raise ConfigError(f"epsilon must be positive, got {self.epsilon}")
+
+    @property
+    def degree(self) -> int:
+        return (self.order - 1) // 2
+
+
+@dataclass(frozen=True)
+class FluxConfig:
+    """Numerical flux choice plus its reconstruction settings (flux.py:57-67)."""
+
+    kind: str = "lf"
+    weno: WenoConfig = field(default_factory=WenoConfig)
+
+    def __post_init__(self):
+        if self.kind not in FLUX_KINDS:
+            raise ConfigError(
+                f"unknown flux kind '{self.kind}', expected one of {FLUX_KINDS}")
+
+
+class SemiDiscreteOperator:
+    """du_i/dt = -(F_{i+1/2} - F_{i-1/2}) / dx on a periodic mesh, with WENO
+    interface states and the global LF flux; fields (..., 1, N)."""
+
+    def __init__(self, model: ConservationModel, space_grid: SpatialGrid,
+                 config: FluxConfig):
+        if space_grid.n_cells < 2 * config.weno.degree + 1:
+            raise ConfigError(f"{space_grid.n_cells} cells cannot support order "
+                              f"{config.weno.order} reconstruction")
+        if config.kind != "lf":
+            raise ConfigError("the B200 path implements the Lax-Friedrichs flux; "
+                              "the Roe flux is out of scope")
+        if getattr(model, "n_components", None) != 1 or not hasattr(model, "abi_model"):
+            raise ConfigError(f"model '{getattr(model, 'kind', model)}' is not a "
+                              "scalar model of the B200 path")
+        self.model = model
+        self.space_grid = space_grid
+        self.config = config
+        self.tables = build_tables(config.weno.degree)
+
+    def phi_struct(self, *, dt: float, rk_order: int, regime: int) -> MgpPhi:
+        return MgpPhi(int(self.model.abi_model), int(self.config.weno.degree),
+                      int(rk_order), int(regime), int(self.space_grid.n_cells),
+                      float(dt), float(self.space_grid.dx),
+                      float(self.config.weno.epsilon), float(self.model.speed))
+
+    def rhs(self, field_):
+        """SemiDiscreteOperator.rhs (flux.py:159-161) on the GPU.  Returns the
+        input's type: NumPy in -> NumPy out, CUDA tensor in -> tensor out."""
+        return apply_phi(self, 0.0, 0, field_)
+
+
+def apply_phi(op: SemiDiscreteOperator, dt: float, rk_order: int, u):
+    """Phi (or the rhs for rk_order 0) on every (1, N) field of u."""
+    is_tensor = torch.is_tensor(u)
+    x = dev.to_device(u)
+    nx = op.space_grid.n_cells
+    if x.dim() < 2 or x.shape[-1] != nx or x.shape[-2] != 1:
+        raise DimensionError(f"expected (..., 1, {nx}) states, got {tuple(x.shape)}")
+    batch = x.numel() // nx
+    out = torch.empty_like(x)
+    if batch:
+        regime = dev.regime_for_batch(batch)
+        dev.sweep(op.phi_struct(dt=dt, rk_order=rk_order, regime=regime),
+                  n_chunks=batch, start=x, start_stride=nx, tail=TAIL_PHI,
+                  tail_regime=regime, tail_out=out, to_s=nx, what="advance")
+    if is_tensor:
+        return out
+    return out.cpu().numpy()
+
+
+def semi_discrete_rhs(model, space_grid, config, field_):
+    """One-shot evaluation of the semi-discrete operator (flux.py:164-167)."""
+    return SemiDiscreteOperator(model, space_grid, config).rhs(field_)

@@ -1,0 +1,528 @@
+"""Multigrid-reduction-in-time on the GPU with C-points-only finest storage.
+
+Same method surface and semantics as reference
+``pkg/src/mgritlab/mgrit.py`` -- ``MgritOptions`` (:50-79),
+``ConvergenceRecord`` (:92-108), ``MgritHierarchy`` with ``f_relax`` /
+``c_relax`` / ``relax`` / ``restrict`` / ``coarse_solve`` / ``interpolate`` /
+``v_cycle`` / ``f_cycle`` / ``run_cycle`` / ``residual_norm`` /
+``fine_values`` (:120-273) and ``mgrit_solve`` (:276-340) -- with every
+propagator application done by the fused kernels of ``libmgrit_phi.so``.
+
+Storage (the B200 design):
+
+* Level 0 keeps only its C-points (nodes 0, m, 2m, ...; N_t/m + 1 states) in
+  two ping-pong buffers.  Its F-points are never stored: they are a pure
+  function of the C-points they were last F-relaxed from (``_fsrc``), or the
+  broadcast initial state before any relaxation.  Every reader of F-points
+  (C-relaxation, restriction, residual, error, ``fine_values``) recomputes
+  them inside its own kernel, bit-identically to the reference's stored
+  values because the same Phi runs in the same summation regime.
+  ``f_relax(0)`` therefore launches nothing.
+* Levels >= 1 keep every node of u and g, as the reference does (level-l
+  F-relaxation adds g at every node).
+
+Chunks of a level are independent inside every launch (mgrit.py:10-15), so
+one launch sweeps all CF-intervals of a level; the coarsest level is one
+persistent CTA marching sequentially.  ``parallelism`` is accepted and has no
+effect: results do not depend on it (the reference's parity baseline is
+parallelism = 1).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import device as dev
+from ._lib import (G_ARRAY, G_NONE, G_ZERO, GUESS_INJECTION, GUESS_LAST_STEP,
+                   SUM_SEQ, TAIL_NONE, TAIL_PHI, TAIL_RESID, TAIL_RESTRICT)
+from .errors import ConfigError, DimensionError
+from .grid import SpatialGrid, TemporalGrid, Trajectory
+from .stepper import RungeKuttaStepper
+
+CYCLE_KINDS = ("v", "f")
+RELAXATION_KINDS = ("f", "fcf")
+GUESS_KINDS = ("injection", "last-step")
+DEFAULT_DIVERGENCE_THRESHOLD = 1e10
+
+
+@dataclass(frozen=True)
+class MgritOptions:
+    """Iteration controls for one multigrid-in-time solve (mgrit.py:50-79)."""
+
+    n_levels: int
+    m: int = 2
+    cycle: str = "v"
+    relaxation: str = "f"
+    guess: str = "last-step"
+    max_iters: int = 10
+    divergence_threshold: float = DEFAULT_DIVERGENCE_THRESHOLD
+    parallelism: int = 1
+
+    def __post_init__(self):
+        if self.n_levels < 2:
+            raise ConfigError(f"need at least 2 levels, got {self.n_levels}")
+        if self.m < 2:
+            raise ConfigError(f"coarsening factor must be >= 2, got {self.m}")
+        if self.cycle not in CYCLE_KINDS:
+            raise ConfigError(f"unknown cycle '{self.cycle}'")
+        if self.relaxation not in RELAXATION_KINDS:
+            raise ConfigError(f"unknown relaxation '{self.relaxation}'")
+        if self.guess not in GUESS_KINDS:
+            raise ConfigError(f"unknown restriction guess '{self.guess}'")
+        if self.max_iters < 0:
+            raise ConfigError(f"max_iters must be >= 0, got {self.max_iters}")
+        if self.divergence_threshold <= 0.0:
+            raise ConfigError("divergence threshold must be positive")
+        if self.parallelism < 1:
+            raise ConfigError(f"parallelism must be >= 1, got {self.parallelism}")
+
+
+@dataclass
+class ConvergenceRecord:
+    """Per-iteration monitoring; row 0 describes the initial iterate
+    (mgrit.py:92-108)."""
+
+    errors: np.ndarray
+    residuals: np.ndarray
+    diverged: bool = False
+    diverged_at: int | None = None
+    converged_at: int | None = None   # first row below residual_tol, if given
+
+    @property
+    def n_iterations(self) -> int:
+        return max(0, len(self.errors) - 1)
+
+
+@dataclass
+class Monitor:
+    """One fused pass over the finest level: residual norm, squared error
+    against a reference trajectory, and the non-finite cell count."""
+
+    residual: float
+    error_sq: float
+    nonfinite: int
+
+
+class MgritLevel:
+    """Per-level view (mgrit.py:82-89).  For l >= 1, ``u`` / ``g`` are the
+    device arrays (n_intervals + 1, 1, N).  For l = 0, ``u`` materialises the
+    full trajectory on demand (a device snapshot) and ``g`` is the implicit
+    finest right-hand side (initial state at node 0, zero elsewhere)."""
+
+    def __init__(self, hierarchy, index, dt, n_intervals, stepper):
+        self._h = hierarchy
+        self.index = index
+        self.dt = dt
+        self.n_intervals = n_intervals
+        self.stepper = stepper
+
+    @property
+    def u(self):
+        if self.index == 0:
+            return self._h.fine_values()
+        return self._h._u[self.index].view(self.n_intervals + 1, 1, -1)
+
+    @property
+    def g(self):
+        if self.index == 0:
+            g = torch.zeros(self.n_intervals + 1, 1, self._h.nx, dtype=dev.DTYPE,
+                            device=self._h.device)
+            g[0, 0] = self._h._u0
+            return g
+        return self._h._g[self.index].view(self.n_intervals + 1, 1, -1)
+
+
+def _check_stepper(s, l: int, nx: int) -> RungeKuttaStepper:
+    if not isinstance(s, RungeKuttaStepper):
+        raise ConfigError(
+            f"level {l}: the B200 hierarchy runs paper_2104_09404_b200."
+            f"RungeKuttaStepper propagators, got {type(s).__name__}")
+    if s.nx != nx:
+        raise DimensionError(f"level {l}: stepper mesh has {s.nx} cells, state has {nx}")
+    return s
+
+
+class MgritHierarchy:
+    """Owns the per-level device arrays and runs cycles over them."""
+
+    def __init__(self, steppers: Sequence, initial_state, time_grid: TemporalGrid,
+                 space_grid: SpatialGrid, options: MgritOptions):
+        L, m = options.n_levels, options.m
+        if len(steppers) != L:
+            raise ConfigError(f"{len(steppers)} steppers supplied for {L} levels")
+        if time_grid.n_steps % (m ** (L - 1)) != 0:
+            raise ConfigError(f"N_t = {time_grid.n_steps} is not divisible by "
+                              f"m^(levels-1) = {m ** (L - 1)}")
+        self.options = options
+        self.time_grid = time_grid
+        self.space_grid = space_grid
+        self.device = dev.device()
+        u0 = dev.to_device(initial_state)
+        if u0.dim() != 2 or u0.shape[0] != 1:
+            raise DimensionError(f"initial state must be (1, N), got {tuple(u0.shape)}")
+        self.nx = nx = u0.shape[1]
+        self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
+        if nx > dev._lib.max_nx():
+            raise ConfigError(f"N_x = {nx} exceeds the single-CTA field limit "
+                              f"{dev._lib.max_nx()} of this build")
+        self._u0 = u0[0].contiguous()
+        self.n = [time_grid.n_steps // m ** l for l in range(L)]
+        self.levels = [MgritLevel(self, l, time_grid.dt * m ** l, self.n[l], steppers[l])
+                       for l in range(L)]
+        n1 = self.n[0] // m
+        self.n_chunks0 = n1
+        kw = dict(dtype=dev.DTYPE, device=self.device)
+        # level 0: C-point ping-pong buffers, rows = C-points 0..n1
+        self._c = [self._u0.expand(n1 + 1, nx).contiguous(), None]
+        self._cur = 0
+        self._fsrc = "ic"        # "ic" (broadcast initial state) or buffer index
+        self._pristine = True    # C-points all equal the initial state
+        # levels >= 1: full u and g
+        self._u = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
+        self._g = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
+        self._phi_buf = torch.empty(max(n1, 1), nx, **kw)
+        self._partials = torch.empty(max(self.n[0] + 1, 1) * 3, **kw)
+        self._sums = torch.empty(4, **kw)
+
+    # -- helpers ------------------------------------------------------------
+
+    def _phi(self, l: int, regime: int):
+        return self.steppers[l].phi_struct(regime)
+
+    def _other(self, i: int) -> int:
+        if self._c[1 - i] is None:
+            self._c[1 - i] = torch.empty_like(self._c[i])
+        return 1 - i
+
+    def _reduce(self, n_chunks: int) -> tuple[float, float, float]:
+        dev.sum_partials(self._partials, n_chunks, 3, self._sums)
+        s = self._sums[:3].cpu().tolist()
+        return s[0], s[1], s[2]
+
+    # -- level operations ----------------------------------------------------
+
+    def f_relax(self, l: int) -> None:
+        """mgrit.py:168-180: u[jm+i] = Phi_l(u[jm+i-1]) + g[jm+i]."""
+        if l == 0:
+            # F-points are implicit: from now on they derive from these C-points
+            self._fsrc = self._cur
+            self._pristine = False
+            return
+        m, nx, n = self.options.m, self.nx, self.n[l]
+        nc = n // m
+        u, g = self._u[l], self._g[l]
+        regime = dev.regime_for_batch(nc)
+        dev.sweep(self._phi(l, regime), n_chunks=nc, start=u, start_stride=m * nx,
+                  n_steps=m - 1, g_mode=G_ARRAY, g=g[1],
+                  g_cs=m * nx, g_ss=nx, store=u[1], st_cs=m * nx, st_ss=nx,
+                  what="f_relax")
+
+    def c_relax(self, l: int) -> None:
+        """mgrit.py:182-191: u[jm] = Phi_l(u[jm-1]) + g[jm]."""
+        m, nx = self.options.m, self.nx
+        if l == 0:
+            nc = self.n_chunks0
+            regime = dev.regime_for_batch(nc)
+            phi = self._phi(0, regime)
+            if self._fsrc == "ic":
+                dst = self._c[self._cur]
+                dev.sweep(phi, n_chunks=nc, start=self._u0, start_stride=0,
+                          tail=TAIL_PHI, tail_regime=regime, tail_g_mode=G_ZERO,
+                          tail_out=dst[1], to_s=nx, what="c_relax")
+            else:
+                src = self._fsrc
+                if self._cur == src:
+                    d = self._other(src)
+                    self._c[d][0].copy_(self._c[src][0])
+                    self._cur = d
+                dst = self._c[self._cur]
+                dev.sweep(phi, n_chunks=nc, start=self._c[src], start_stride=nx,
+                          n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
+                          tail_regime=regime, tail_g_mode=G_ZERO, tail_out=dst[1],
+                          to_s=nx, what="c_relax")
+            self._pristine = False
+            return
+        n = self.n[l]
+        nc = n // m
+        u, g = self._u[l], self._g[l]
+        regime = dev.regime_for_batch(nc)
+        dev.sweep(self._phi(l, regime), n_chunks=nc, start=u[m - 1],
+                  start_stride=m * nx, tail=TAIL_PHI, tail_regime=regime,
+                  tail_g_mode=G_ARRAY, tail_g=g[m], tg_s=m * nx, tail_out=u[m],
+                  to_s=m * nx, what="c_relax")
+
+    def relax(self, l: int) -> None:
+        self.f_relax(l)
+        if self.options.relaxation == "fcf":
+            self.c_relax(l)
+            self.f_relax(l)
+
+    def restrict(self, l: int) -> None:
+        """mgrit.py:199-217: FAS restriction with last-step or injection guess."""
+        m, nx = self.options.m, self.nx
+        nc = self.n[l + 1]
+        regime = dev.regime_for_batch(nc)
+        cu, cg = self._u[l + 1], self._g[l + 1]
+        phi_buf = self._phi_buf
+        guess = GUESS_LAST_STEP if self.options.guess == "last-step" else GUESS_INJECTION
+        if l == 0:
+            cpts = self._c[self._cur]
+            cg[0].copy_(cpts[0])
+            cu[0].copy_(cpts[0])
+            # phi_fine = Phi_0(u[mi-1]): recompute the last F-point of chunk i-1
+            if self._fsrc == "ic":
+                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._u0,
+                          start_stride=0, tail=TAIL_PHI, tail_regime=regime,
+                          tail_out=phi_buf, to_s=nx, what="restrict/fine")
+            else:
+                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._c[self._fsrc],
+                          start_stride=nx, n_steps=m - 1, g_mode=G_ZERO,
+                          tail=TAIL_PHI, tail_regime=regime, tail_out=phi_buf,
+                          to_s=nx, what="restrict/fine")
+            # psi = Phi_1(u[m(i-1)]) and the FAS combination
+            dev.sweep(self._phi(1, regime), n_chunks=nc, start=cpts, start_stride=nx,
+                      tail=TAIL_RESTRICT, tail_regime=regime, tail_g_mode=G_ZERO,
+                      guess=guess, aux=phi_buf, aux_s=nx, aux2=cpts[1], aux2_s=nx,
+                      tail_out=cg[1], to_s=nx, tail_out2=cu[1], to2_s=nx,
+                      what="restrict/coarse")
+            return
+        fu, fg = self._u[l], self._g[l]
+        cg[0].copy_(fu[0])
+        cu[0].copy_(fu[0])
+        dev.sweep(self._phi(l, regime), n_chunks=nc, start=fu[m - 1],
+                  start_stride=m * nx, tail=TAIL_PHI, tail_regime=regime,
+                  tail_out=phi_buf, to_s=nx, what="restrict/fine")
+        dev.sweep(self._phi(l + 1, regime), n_chunks=nc, start=fu, start_stride=m * nx,
+                  tail=TAIL_RESTRICT, tail_regime=regime, tail_g_mode=G_ARRAY,
+                  tail_g=fg[m], tg_s=m * nx, guess=guess, aux=phi_buf, aux_s=nx,
+                  aux2=fu[m], aux2_s=m * nx, tail_out=cg[1], to_s=nx,
+                  tail_out2=cu[1], to2_s=nx, what="restrict/coarse")
+
+    def coarse_solve(self) -> None:
+        """mgrit.py:219-226: sequential single-state solve of the coarsest
+        level -- one persistent CTA marches every step."""
+        L = self.options.n_levels
+        nx = self.nx
+        u, g = self._u[L - 1], self._g[L - 1]
+        n = self.n[L - 1]
+        dev.sweep(self._phi(L - 1, dev.regime_for_batch(1)), n_chunks=1, start=u,
+                  start_stride=0, n_steps=n, g_mode=G_ARRAY, g=g[1], g_ss=nx,
+                  store=u[1], st_ss=nx, what="coarse_solve")
+
+    def interpolate(self, l: int) -> None:
+        """mgrit.py:228-232: inject level l+1 onto level l's C-points, F-relax."""
+        m = self.options.m
+        if l == 0:
+            self._c[self._cur].copy_(self._u[1])
+            self._pristine = False
+        else:
+            self._u[l][::m].copy_(self._u[l + 1])
+        self.f_relax(l)
+
+    # -- cycles ----------------------------------------------------------------
+
+    def v_cycle(self, l: int = 0) -> None:
+        if l == self.options.n_levels - 1:
+            self.coarse_solve()
+            return
+        self.relax(l)
+        self.restrict(l)
+        self.v_cycle(l + 1)
+        self.interpolate(l)
+
+    def f_cycle(self) -> None:
+        L = self.options.n_levels
+        for l in range(L - 1):
+            self.relax(l)
+            self.restrict(l)
+        self.coarse_solve()
+        for l in range(L - 2, -1, -1):
+            self.interpolate(l)
+            if l > 0:
+                self.v_cycle(l)
+
+    def run_cycle(self) -> None:
+        if self.options.cycle == "f":
+            self.f_cycle()
+        else:
+            self.v_cycle(0)
+
+    # -- monitoring --------------------------------------------------------------
+
+    def _fast_monitor_ok(self) -> bool:
+        return (self._fsrc == self._cur
+                and dev.regime_for_batch(self.n_chunks0) == SUM_SEQ)
+
+    def monitor(self, reference: torch.Tensor | None = None) -> Monitor:
+        """Residual norm (mgrit.py:264-270), squared error against
+        ``reference`` rows (grid.py:96-108 numerator) and the number of
+        non-finite cells of the finest iterate (mgrit.py:323), in one pass."""
+        m, nx, nt = self.options.m, self.nx, self.n[0]
+        ref = None if reference is None else reference.reshape(nt + 1, nx)
+        resid_regime = dev.regime_for_batch(nt)
+        if self._pristine and self._fsrc == "ic":
+            # every node holds u0: r = (0 + Phi(u0)) - u0 at each of the Nt nodes
+            dev.sweep(self._phi(0, resid_regime), n_chunks=1, start=self._u0,
+                      start_stride=0, tail=TAIL_RESID, tail_regime=resid_regime,
+                      tail_g_mode=G_ZERO, aux=self._u0, aux_s=0,
+                      partials=self._partials, what="residual")
+            r2, _, _ = self._reduce(1)
+            dev.sweep(self._phi(0, resid_regime), n_chunks=nt + 1, start=self._u0,
+                      start_stride=0, ref=ref, ref_cs=nx, count_nonfinite=1,
+                      partials=self._partials, what="monitor")
+            _, e2, nf = self._reduce(nt + 1)
+            return Monitor(math.sqrt(nt * r2), e2, int(nf))
+        if self._fast_monitor_ok():
+            # F-point residuals are exactly zero (same Phi, same regime as the
+            # F-relaxation that defines them); C-point residuals need the
+            # recomputed last F-point of each chunk.
+            nc = self.n_chunks0
+            c = self._c[self._cur]
+            dev.sweep(self._phi(0, dev.regime_for_batch(nc)), n_chunks=nc, start=c,
+                      start_stride=nx, n_steps=m - 1, g_mode=G_ZERO, ref=ref,
+                      ref_cs=m * nx, ref_ss=nx, ref_last_next=1, count_nonfinite=1,
+                      tail=TAIL_RESID, tail_regime=resid_regime, tail_g_mode=G_ZERO,
+                      aux=c[1], aux_s=nx, partials=self._partials, what="monitor")
+            r2, e2, nf = self._reduce(nc)
+            return Monitor(math.sqrt(r2), e2, int(nf))
+        # general state: materialise the trajectory, then one batched pass
+        traj = self.fine_values().reshape(nt + 1, nx)
+        dev.sweep(self._phi(0, resid_regime), n_chunks=nt, start=traj,
+                  start_stride=nx, ref=ref, ref_cs=nx, count_nonfinite=1,
+                  tail=TAIL_RESID, tail_regime=resid_regime, tail_g_mode=G_ZERO,
+                  aux=traj[1], aux_s=nx, ref_last_next=1, partials=self._partials,
+                  what="monitor")
+        r2, e2, nf = self._reduce(nt)
+        return Monitor(math.sqrt(r2), e2, int(nf))
+
+    def residual_norm(self) -> float:
+        """Euclidean norm of the finest-level residual g + Phi(u_prev) - u."""
+        return self.monitor().residual
+
+    def fine_values(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """The finest-level trajectory (N_t + 1, 1, N) as a device tensor,
+        F-points recomputed from the C-points they derive from (written into
+        ``out`` when given)."""
+        m, nx, nt = self.options.m, self.nx, self.n[0]
+        if out is None:
+            out = torch.empty(nt + 1, nx, dtype=dev.DTYPE, device=self.device)
+        else:
+            out = out.view(nt + 1, nx)
+        out[::m].copy_(self._c[self._cur])
+        nc = self.n_chunks0
+        if self._fsrc == "ic":
+            for s in range(1, m):
+                out[s::m].copy_(self._u0.expand(nc, nx))
+        else:
+            dev.sweep(self._phi(0, dev.regime_for_batch(nc)), n_chunks=nc,
+                      start=self._c[self._fsrc], start_stride=nx, n_steps=m - 1,
+                      g_mode=G_ZERO, store=out[1], st_cs=m * nx, st_ss=nx,
+                      what="fine_values")
+        return out.view(nt + 1, 1, nx)
+
+    def load_c_points(self, c_points) -> None:
+        """Set the finest-level C-points (N_t/m + 1 rows, host or device) and
+        take the F-points as F-relaxed from them (the state after an
+        interpolation).  Host tensors are copied asynchronously (pinned
+        memory recommended)."""
+        c = self._c[self._cur]
+        src = c_points if torch.is_tensor(c_points) else torch.from_numpy(
+            np.ascontiguousarray(c_points, dtype=np.float64))
+        c.copy_(src.reshape(c.shape), non_blocking=True)
+        self._fsrc = self._cur
+        self._pristine = False
+
+    def c_points(self) -> torch.Tensor:
+        """Current finest-level C-points (N_t/m + 1, 1, N), device view."""
+        return self._c[self._cur].view(-1, 1, self.nx)
+
+
+def _ref_norm_sq(reference: torch.Tensor, nx: int, stepper) -> float:
+    """||reference||^2 with the same deterministic reduction as the error."""
+    rows = reference.numel() // nx
+    zero = torch.zeros(nx, dtype=dev.DTYPE, device=reference.device)
+    partials = torch.empty(rows * 3, dtype=dev.DTYPE, device=reference.device)
+    sums = torch.empty(4, dtype=dev.DTYPE, device=reference.device)
+    dev.sweep(stepper.phi_struct(SUM_SEQ), n_chunks=rows, start=zero, start_stride=0,
+              ref=reference.reshape(rows, nx), ref_cs=nx, partials=partials,
+              what="reference norm")
+    dev.sum_partials(partials, rows, 3, sums)
+    return float(sums[1].item())
+
+
+def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
+                space_grid: SpatialGrid, options: MgritOptions, reference=None,
+                *, return_trajectory: bool = True, hierarchy_out: list | None = None,
+                residual_tol: float | None = None):
+    """Iterate cycles until max_iters, recording convergence per iteration
+    (mgrit.py:276-340): row 0 is the initial iterate; divergence (non-finite
+    iterate, or relative error above the threshold, or a non-finite error
+    when a reference is supplied) is recorded, not raised, and that row plus
+    all later rows stay NaN.
+
+    reference: serial trajectory (N_t + 1, 1, N), host array or CUDA tensor.
+    Returns (Trajectory, ConvergenceRecord); the trajectory values are a host
+    array (``return_trajectory=False`` skips materialising it, e.g. for
+    problems whose full trajectory does not fit in memory).  residual_tol
+    (not in the reference, BASELINE config 1 "stop at residual < 1e-10")
+    stops after the first row whose residual is below it.
+    """
+    h = MgritHierarchy(steppers, initial_state, time_grid, space_grid, options)
+    if hierarchy_out is not None:
+        hierarchy_out.append(h)
+
+    def trajectory():
+        if not return_trajectory:
+            return None
+        return Trajectory(time_grid, space_grid, h.fine_values().cpu().numpy())
+
+    if options.max_iters == 0:
+        return trajectory(), ConvergenceRecord(errors=np.empty(0), residuals=np.empty(0))
+
+    ref = None
+    ref_norm = None
+    if reference is not None:
+        ref = dev.to_device(reference)
+        if ref.numel() != (time_grid.n_steps + 1) * h.nx:
+            raise DimensionError(f"reference has shape {tuple(ref.shape)}")
+        ref_norm = math.sqrt(_ref_norm_sq(ref, h.nx, h.steppers[0]))
+        if ref_norm == 0.0:
+            raise ValueError("reference trajectory has zero norm")
+
+    def error(mon: Monitor) -> float:
+        if ref is None:
+            return math.nan
+        return math.sqrt(mon.error_sq) / ref_norm
+
+    n_rows = options.max_iters + 1
+    errors = np.full(n_rows, np.nan)
+    residuals = np.full(n_rows, np.nan)
+    diverged, diverged_at, converged_at = False, None, None
+    mon = h.monitor(ref)
+    errors[0] = error(mon)
+    residuals[0] = mon.residual
+    for it in range(1, n_rows):
+        if residual_tol is not None and converged_at is not None:
+            break
+        h.run_cycle()
+        mon = h.monitor(ref)
+        err = error(mon)
+        finite = mon.nonfinite == 0
+        if not finite or (np.isfinite(err) and err > options.divergence_threshold):
+            diverged, diverged_at = True, it
+            break
+        if ref is not None and not np.isfinite(err):
+            diverged, diverged_at = True, it
+            break
+        errors[it] = err
+        residuals[it] = mon.residual
+        if residual_tol is not None and converged_at is None and mon.residual < residual_tol:
+            converged_at = it
+    record = ConvergenceRecord(errors=errors, residuals=residuals,
+                               diverged=diverged, diverged_at=diverged_at,
+                               converged_at=converged_at)
+    return trajectory(), record

@@ -1,0 +1,108 @@
+"""Scalar conservation-law models of the GPU path.
+
+``Burgers`` mirrors reference ``pkg/src/mgritlab/models.py:101-133`` (flux
+(0.5 u) u, eigenvalue u, max speed |u|).  ``Advection`` is the linear model
+BASELINE.json config 1 needs (u_t + a u_x = 0, flux a u, |lambda| = |a|);
+the reference rejects "advection" (tests/test_models.py:197-198), so it is a
+new ``ConservationModel`` subclass with the same shape contract.  The
+systems (shallow water, Euler, models.py:136-308) are outside the GPU path's
+scope: ``make_model`` raises ConfigError for them.
+
+These host methods are the reference's NumPy semantics for callers and
+tests; the device kernels implement the same formulas (csrc/mgrit_phi.cu).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import ConfigError, DimensionError
+
+MODEL_BURGERS = 0    # MGP_MODEL_BURGERS
+MODEL_ADVECTION = 1  # MGP_MODEL_ADVECTION
+
+
+class ConservationModel:
+    """Common interface (models.py:61-98)."""
+
+    kind: str
+    n_components: int
+    abi_model: int
+
+    def _check_shape(self, u) -> None:
+        if u.ndim < 2 or u.shape[-2] != self.n_components:
+            raise DimensionError(
+                f"{self.kind} expects (..., {self.n_components}, N) states, "
+                f"got shape {u.shape}")
+
+    def flux(self, u):
+        raise NotImplementedError
+
+    def eigenvalues(self, u):
+        raise NotImplementedError
+
+    def max_abs_speed(self, u):
+        return np.max(np.abs(self.eigenvalues(u)), axis=-1)
+
+
+class Burgers(ConservationModel):
+    """Scalar model with flux u^2/2; the single wave moves at speed u."""
+
+    kind = "burgers"
+    n_components = 1
+    abi_model = MODEL_BURGERS
+    speed = 0.0
+
+    def flux(self, u):
+        self._check_shape(u)
+        return 0.5 * u * u
+
+    def eigenvalues(self, u):
+        self._check_shape(u)
+        return np.moveaxis(u, -2, -1)
+
+    def max_abs_speed(self, u):
+        self._check_shape(u)
+        return np.abs(u[..., 0, :])
+
+
+class Advection(ConservationModel):
+    """Linear advection u_t + a u_x = 0 with constant speed a."""
+
+    kind = "advection"
+    n_components = 1
+    abi_model = MODEL_ADVECTION
+
+    def __init__(self, speed: float = 1.0):
+        speed = float(speed)
+        if not np.isfinite(speed):
+            raise ConfigError(f"advection speed must be finite, got {speed}")
+        self.speed = speed
+
+    def flux(self, u):
+        self._check_shape(u)
+        return self.speed * u
+
+    def eigenvalues(self, u):
+        self._check_shape(u)
+        return np.full(np.moveaxis(u, -2, -1).shape, self.speed)
+
+    def max_abs_speed(self, u):
+        self._check_shape(u)
+        return np.full(u[..., 0, :].shape, abs(self.speed))
+
+
+_MODEL_KINDS = ("burgers", "advection")
+_OUT_OF_SCOPE = ("shallow-water", "euler")
+
+
+def make_model(kind: str, *, speed: float = 1.0, **_unused) -> ConservationModel:
+    """Build a model by name (models.py:318-328 plus "advection")."""
+    if kind == "burgers":
+        return Burgers()
+    if kind == "advection":
+        return Advection(speed)
+    if kind in _OUT_OF_SCOPE:
+        raise ConfigError(
+            f"model '{kind}' is a system; the B200 path implements the scalar "
+            f"models {_MODEL_KINDS} only")
+    raise ConfigError(f"unknown model '{kind}', expected one of {sorted(_MODEL_KINDS)}")

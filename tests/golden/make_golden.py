@@ -1,0 +1,318 @@
+"""Generate the golden fixtures from the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports the unmodified reference package (``/root/reference/pkg/src``,
+``mgritlab``) read-only, runs its own ``RungeKuttaStepper.advance``,
+``SemiDiscreteOperator.rhs`` and ``mgrit_solve`` / ``solve_serial`` on seeded
+inputs, and writes
+
+* ``phi_vectors.npz``  -- inputs/outputs of the propagator for every
+  (model, WENO degree, RK order, batch regime) combination, including shock
+  fields and non-finite cells;
+* ``mgrit_cases.npz`` + ``mgrit_cases.json`` -- residual / error histories,
+  divergence rows and (small cases) final trajectories of MGRIT runs on
+  scaled BASELINE configurations and on checked-in reference configs
+  (pkg/configs/high_order_burgers_lf.cfg, order_mix_*_lf.cfg).
+
+The linear-advection model BASELINE config 1 needs is not in the reference
+(tests/test_models.py:197-198 rejects it); it is added here as a subclass of
+the reference's own ``ConservationModel`` (flux a*u, |lambda| = |a|).  The
+GPU box has no /root/reference: the tests read only these committed files.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF_SRC = "/root/reference/pkg/src"
+sys.path.insert(0, REF_SRC)
+sys.path.insert(0, ROOT)
+
+import mgritlab as R  # noqa: E402  (the reference)
+from mgritlab.models import ConservationModel  # noqa: E402
+
+import oracle  # noqa: E402
+from oracle import mgrit_oracle  # noqa: E402
+from paper_2104_09404_b200 import harness as H  # noqa: E402  (IC helpers only)
+
+
+class RefAdvection(ConservationModel):
+    """u_t + a u_x = 0 with the reference model interface (models.py:61-98)."""
+
+    kind = "advection"
+    n_components = 1
+
+    def __init__(self, speed=1.0):
+        self.speed = float(speed)
+
+    def flux(self, u):
+        self._check_shape(u)
+        return self.speed * u
+
+    def eigenvalues(self, u):
+        self._check_shape(u)
+        return np.full(np.moveaxis(u, -2, -1).shape, self.speed)
+
+    def max_abs_speed(self, u):
+        self._check_shape(u)
+        return np.full(u[..., 0, :].shape, abs(self.speed))
+
+
+def ref_model(name, speed=1.0):
+    return RefAdvection(speed) if name == "advection" else R.make_model(name)
+
+
+def ref_stepper(model, sg, k, rk, dt, eps=1e-6):
+    op = R.SemiDiscreteOperator(model, sg, R.FluxConfig("lf", R.WenoConfig(
+        order=2 * k + 1, epsilon=eps)))
+    return op, R.RungeKuttaStepper(op.rhs, dt, max(rk, 1))
+
+
+# ---------------------------------------------------------------------------
+# propagator vectors
+# ---------------------------------------------------------------------------
+
+def make_fields(rng, shape, kind):
+    nx = shape[-1]
+    x = (np.arange(nx) + 0.5) / nx
+    base = 0.5 + 0.3 * np.sin(2 * np.pi * x) + 0.1 * rng.standard_normal(shape)
+    if kind == "shock":
+        base = base + np.where(x > 0.4, -0.8, 0.4)
+    elif kind == "rough":
+        base = rng.standard_normal(shape)
+    elif kind == "nan":
+        base = base.copy()
+        base[..., nx // 3] = np.nan
+    elif kind == "inf":
+        base = base.copy()
+        base[..., 2] = np.inf
+    elif kind == "huge":
+        base = base.copy()
+        base[..., 5] = 1e200
+    return np.ascontiguousarray(base, dtype=np.float64)
+
+
+def phi_vectors():
+    rng = np.random.default_rng(20210419)
+    out = {}
+    index = []
+    n = 0
+    for model_name in ("burgers", "advection"):
+        for k in (0, 1, 2, 3):
+            for rk in (0, 1, 2, 3):
+                for shape_kind, shape in (("batch", (3, 1, 32)), ("single", (1, 32))):
+                    kinds = ["smooth", "shock", "rough"]
+                    if rk == 3 and shape_kind == "batch":
+                        kinds += ["nan", "inf", "huge"]
+                    for fk in kinds:
+                        u = make_fields(rng, shape, fk)
+                        nx = shape[-1]
+                        sg = R.SpatialGrid(1.0, nx)
+                        model = ref_model(model_name, speed=-0.75 if model_name == "advection" else 1.0)
+                        dt = 0.35 * sg.dx
+                        op, st = ref_stepper(model, sg, k, rk, dt)
+                        with np.errstate(all="ignore"):
+                            y = op.rhs(u) if rk == 0 else st.advance(u)
+                        # the oracle must agree bit for bit (NaN-aware)
+                        p = oracle.make_params(model=model_name, k=k, rk_order=rk,
+                                               dt=dt, dx=sg.dx, speed=model.speed
+                                               if model_name == "advection" else 1.0,
+                                               regime=oracle.regime_for_shape(shape))
+                        mine = oracle.phi_apply(p, u)
+                        assert np.array_equal(mine, y, equal_nan=True), (model_name, k, rk, shape, fk)
+                        key = f"v{n:04d}"
+                        out[key + "_in"] = u
+                        out[key + "_out"] = y
+                        index.append(dict(key=key, model=model_name, k=k, rk=rk,
+                                          shape=list(shape), field=fk, dt=dt, dx=sg.dx,
+                                          speed=float(model.speed) if model_name == "advection" else 1.0,
+                                          eps=1e-6))
+                        n += 1
+    # one production-shaped case: WENO5 / SSP-RK3 Burgers, nx = 512
+    sg = R.SpatialGrid(1.0, 512)
+    u = make_fields(rng, (4, 1, 512), "shock")
+    op, st = ref_stepper(R.make_model("burgers"), sg, 2, 3, 0.4 * sg.dx)
+    key = f"v{n:04d}"
+    out[key + "_in"] = u
+    out[key + "_out"] = st.advance(u)
+    index.append(dict(key=key, model="burgers", k=2, rk=3, shape=[4, 1, 512],
+                      field="shock", dt=0.4 * sg.dx, dx=sg.dx, speed=1.0, eps=1e-6))
+    np.savez_compressed(os.path.join(HERE, "phi_vectors.npz"), **out)
+    with open(os.path.join(HERE, "phi_vectors.json"), "w") as f:
+        json.dump(index, f, indent=0)
+    print(f"phi vectors: {len(index)}")
+
+
+# ---------------------------------------------------------------------------
+# MGRIT histories
+# ---------------------------------------------------------------------------
+
+_RK = {"fe": 1, "ssprk2": 2, "ssprk3": 3}
+
+
+def case_ic(spec):
+    sg = R.SpatialGrid(spec.get("length", 1.0), spec["n_x"])
+    ic = spec["ic"]
+    if ic == "fourier":
+        return H.fourier_ic(H.SpatialGrid(spec.get("length", 1.0), spec["n_x"]),
+                            spec["n_modes"], spec.get("seed", 1234), spec.get("decay", False))
+    if ic == "sine":
+        return H.sine_ic(H.SpatialGrid(1.0, spec["n_x"]))
+    return R.initial_state(ic, sg, spec.get("length", 1.0))
+
+
+def case_horizon(spec, u0):
+    if "horizon" in spec:
+        return spec["horizon"]
+    sg = R.SpatialGrid(spec.get("length", 1.0), spec["n_x"])
+    speed = abs(spec.get("speed", 1.0)) if spec["model"] == "advection" else float(np.max(np.abs(u0)))
+    return H.cfl_horizon(spec["n_t"], spec["cfl"], sg.dx, speed)
+
+
+def run_reference(spec):
+    u0 = case_ic(spec)
+    sg = R.SpatialGrid(spec.get("length", 1.0), spec["n_x"])
+    tg = R.TemporalGrid(case_horizon(spec, u0), spec["n_t"])
+    model = ref_model(spec["model"], spec.get("speed", 1.0))
+    L, m = spec["n_levels"], spec["m"]
+    orders = spec["weno_order"] * (L if len(spec["weno_order"]) == 1 else 1)
+    kinds = spec["stepper"] * (L if len(spec["stepper"]) == 1 else 1)
+    steppers = []
+    for l in range(L):
+        op = R.SemiDiscreteOperator(model, sg, R.FluxConfig("lf", R.WenoConfig(
+            order=orders[l], epsilon=spec.get("epsilon", 1e-6))))
+        steppers.append(R.RungeKuttaStepper(op.rhs, tg.dt * m ** l, _RK[kinds[l]]))
+    opts = R.MgritOptions(n_levels=L, m=m, cycle=spec["cycle"],
+                          relaxation=spec["relaxation"], guess=spec["guess"],
+                          max_iters=spec["max_iters"])
+    reference = None
+    serial = None
+    if spec["semantics"] == "harness":
+        serial = R.solve_serial(steppers[0], u0, tg, sg, model)
+        reference = serial.trajectory.values
+    traj, rec = R.mgrit_solve(steppers, u0, tg, sg, opts, reference=reference)
+    # cross-check: the oracle restatement of mgrit.py with oracle steppers
+    o_steppers = []
+    for l in range(L):
+        o_steppers.append(oracle.OracleStepper(
+            model=spec["model"], k=(orders[l] - 1) // 2, rk_order=_RK[kinds[l]],
+            dt=tg.dt * m ** l, dx=sg.dx, eps=spec.get("epsilon", 1e-6),
+            speed=spec.get("speed", 1.0), nthreads=1))
+    o_ref = None
+    if reference is not None:
+        o_ref = mgrit_oracle.march(o_steppers[0], u0, spec["n_t"])
+        assert np.array_equal(o_ref, reference)
+    o_opts = mgrit_oracle.Options(n_levels=L, m=m, cycle=spec["cycle"],
+                                  relaxation=spec["relaxation"], guess=spec["guess"],
+                                  max_iters=spec["max_iters"])
+    o_traj, o_rec = mgrit_oracle.mgrit_solve(o_steppers, u0, spec["n_t"], tg.dt, o_opts,
+                                             reference=o_ref)
+    assert o_rec.diverged_at == rec.diverged_at, (spec["name"], o_rec.diverged_at, rec.diverged_at)
+    assert np.array_equal(o_traj, traj.values, equal_nan=True), spec["name"]
+    ok = np.isfinite(rec.residuals)
+    assert np.allclose(o_rec.residuals[ok], rec.residuals[ok], rtol=1e-12, atol=0), spec["name"]
+    return u0, tg, rec, traj.values, (serial.trajectory.values if serial else None)
+
+
+CASES = [
+    # BASELINE config 1 at full size (advection, upwind-as-LF, FE, m=8, L=2)
+    dict(name="c1_fcf_residual_only", model="advection", speed=1.0, n_x=128, n_t=1024,
+         cfl=0.5, ic="sine", weno_order=[1], stepper=["fe"], n_levels=2, m=8, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=66, semantics="residual"),
+    dict(name="c1_f_residual_only", model="advection", speed=1.0, n_x=128, n_t=1024,
+         cfl=0.5, ic="sine", weno_order=[1], stepper=["fe"], n_levels=2, m=8, cycle="v",
+         relaxation="f", guess="last-step", max_iters=130, semantics="residual"),
+    dict(name="c1_fcf_harness", model="advection", speed=1.0, n_x=128, n_t=1024,
+         cfl=0.5, ic="sine", weno_order=[1], stepper=["fe"], n_levels=2, m=8, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=3, semantics="harness"),
+    # BASELINE config 2 shape, scaled (WENO5 / SSP-RK3 Burgers, m=4, L=2, FCF)
+    dict(name="c2_scaled", model="burgers", n_x=64, n_t=256, cfl=0.4, ic="fourier",
+         n_modes=4, weno_order=[5], stepper=["ssprk3"], n_levels=2, m=4, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=4, semantics="harness"),
+    dict(name="c2_scaled_converging", model="burgers", n_x=64, n_t=256, cfl=0.05,
+         ic="fourier", n_modes=4, weno_order=[5], stepper=["ssprk3"], n_levels=2, m=4,
+         cycle="v", relaxation="fcf", guess="last-step", max_iters=12, semantics="harness"),
+    # BASELINE config 3 shape, scaled (multilevel V-cycle, m=4, <=16 coarse steps)
+    dict(name="c3_scaled", model="burgers", n_x=64, n_t=1024, cfl=0.005, ic="fourier",
+         n_modes=8, weno_order=[5], stepper=["ssprk3"], n_levels=4, m=4, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=8, semantics="harness"),
+    dict(name="c3_scaled_divergent", model="burgers", n_x=64, n_t=1024, cfl=0.4,
+         ic="fourier", n_modes=8, weno_order=[5], stepper=["ssprk3"], n_levels=4, m=4,
+         cycle="v", relaxation="fcf", guess="last-step", max_iters=3, semantics="harness"),
+    # BASELINE config 4 style cases (3 levels, F and FCF, WENO1/3/5, RK2/3)
+    dict(name="c4_weno5_rk3_fcf", model="burgers", n_x=32, n_t=512, cfl=0.1, ic="fourier",
+         n_modes=4, weno_order=[5], stepper=["ssprk3"], n_levels=3, m=2, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=14, semantics="residual"),
+    dict(name="c4_weno3_rk2_f", model="burgers", n_x=32, n_t=512, cfl=0.1, ic="fourier",
+         n_modes=4, weno_order=[3], stepper=["ssprk2"], n_levels=3, m=2, cycle="v",
+         relaxation="f", guess="last-step", max_iters=14, semantics="residual"),
+    dict(name="c4_weno1_rk3_f", model="burgers", n_x=32, n_t=512, cfl=0.2, ic="fourier",
+         n_modes=4, weno_order=[1], stepper=["ssprk3"], n_levels=3, m=2, cycle="v",
+         relaxation="f", guess="last-step", max_iters=10, semantics="residual"),
+    # BASELINE config 5 shape, scaled (16 modes a_k/k, m=16)
+    dict(name="c5_scaled", model="burgers", n_x=32, n_t=4096, cfl=0.4, ic="fourier",
+         n_modes=16, decay=True, weno_order=[5], stepper=["ssprk3"], n_levels=3, m=16,
+         cycle="v", relaxation="fcf", guess="last-step", max_iters=2, semantics="residual"),
+    # F-cycle + injection guess
+    dict(name="fcycle_injection", model="burgers", n_x=32, n_t=256, cfl=0.1, ic="fourier",
+         n_modes=4, weno_order=[3], stepper=["ssprk2"], n_levels=4, m=2, cycle="f",
+         relaxation="f", guess="injection", max_iters=8, semantics="harness"),
+    dict(name="fcycle_fcf_laststep", model="burgers", n_x=32, n_t=256, cfl=0.1, ic="fourier",
+         n_modes=4, weno_order=[5], stepper=["ssprk3"], n_levels=3, m=2, cycle="f",
+         relaxation="fcf", guess="last-step", max_iters=8, semantics="harness"),
+    # single chunk on the finest level (2-lane regime there, general residual path)
+    dict(name="single_chunk", model="burgers", n_x=16, n_t=4, cfl=0.3, ic="fourier",
+         n_modes=2, weno_order=[5], stepper=["ssprk3"], n_levels=2, m=4, cycle="v",
+         relaxation="fcf", guess="last-step", max_iters=3, semantics="harness"),
+    # checked-in reference configs (pkg/configs/*.cfg, LF flux, RK steppers)
+    *[dict(name=f"high_order_burgers_lf_w{o}", model="burgers", n_x=64, n_t=400,
+           horizon=0.5, ic="burgers-43", weno_order=[o], stepper=["ssprk3"], n_levels=3,
+           m=2, cycle="v", relaxation="f", guess="last-step", max_iters=10,
+           semantics="harness") for o in (1, 3, 5, 7)],
+    *[dict(name=f"order_mix_space_lf_{'_'.join(map(str, o))}", model="burgers", n_x=64,
+           n_t=400, horizon=0.5, ic="burgers-43", weno_order=list(o), stepper=["ssprk3"],
+           n_levels=3, m=2, cycle="v", relaxation="f", guess="last-step", max_iters=10,
+           semantics="harness") for o in ((3, 5, 7), (7, 5, 3))],
+    dict(name="order_mix_space_time_down_lf", model="burgers", n_x=64, n_t=400,
+         horizon=0.5, ic="burgers-43", weno_order=[7, 5, 3],
+         stepper=["ssprk3", "ssprk2", "fe"], n_levels=3, m=2, cycle="v", relaxation="f",
+         guess="last-step", max_iters=10, semantics="harness"),
+    dict(name="order_mix_space_time_up_lf", model="burgers", n_x=64, n_t=400,
+         horizon=0.5, ic="burgers-43", weno_order=[3, 5, 7],
+         stepper=["fe", "ssprk2", "ssprk3"], n_levels=3, m=2, cycle="v", relaxation="f",
+         guess="last-step", max_iters=10, semantics="harness"),
+]
+
+
+def mgrit_cases():
+    arrays = {}
+    meta = []
+    for spec in CASES:
+        u0, tg, rec, traj, serial = run_reference(spec)
+        key = spec["name"]
+        arrays[key + "__u0"] = u0
+        arrays[key + "__errors"] = rec.errors
+        arrays[key + "__residuals"] = rec.residuals
+        if traj.size <= 40000:
+            arrays[key + "__traj"] = traj
+        m = dict(spec)
+        m.update(horizon=tg.horizon, dt=tg.dt, diverged=bool(rec.diverged),
+                 diverged_at=rec.diverged_at, has_traj=bool(traj.size <= 40000))
+        meta.append(m)
+        print(f"{key}: diverged_at={rec.diverged_at} resid[:3]={rec.residuals[:3]}")
+    np.savez_compressed(os.path.join(HERE, "mgrit_cases.npz"), **arrays)
+    with open(os.path.join(HERE, "mgrit_cases.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
+if __name__ == "__main__":
+    phi_vectors()
+    mgrit_cases()
