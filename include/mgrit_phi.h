@@ -108,6 +108,9 @@ typedef struct mgp_phi {
  *   partials (if non-NULL): [3b+0] residual^2, [3b+1] error^2 (ref non-NULL),
  *   [3b+2] number of non-finite cells seen (when count_nonfinite != 0).
  *
+ * When n_steps > 0 and tail != MGP_TAIL_NONE, tail_regime must equal
+ * phi.regime (each launch runs in one summation regime).
+ *
  * n_chunks = 1 with store of every step is the sequential coarse solve /
  * serial march.  Chunks never read rows another chunk writes in the same
  * call (the caller guarantees it, e.g. by writing new C-points to a

@@ -17,7 +17,7 @@ from .errors import ConfigError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "libmgrit_phi.so")
+LIB_PATH = os.environ.get("MGP_LIB_PATH") or os.path.join(_PKG, "libmgrit_phi.so")
 SRC_PATH = os.path.join(_PKG, "csrc", "mgrit_phi.cu")
 HEADER_PATH = os.path.join(_ROOT, "include", "mgrit_phi.h")
 

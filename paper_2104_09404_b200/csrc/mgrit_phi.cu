@@ -17,9 +17,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/mgrit_phi.h"
+#include "div_shared.cuh"
 
 // ---------------------------------------------------------------------------
 // WENO tables (weno.py:43-86): numerators over a common denominator; the
@@ -78,9 +80,13 @@ __constant__ double c_sm[4][4][4][4] = MGP_SM_TABLE;
 
 namespace {
 
+using mgp::SharedRcp;
+using mgp::div_shared;
+using mgp::shared_rcp;
+
 constexpr int kMaxThreads = 512;
-constexpr int kMaxPerThread = 8;
-constexpr int64_t kMaxNx = (int64_t)kMaxThreads * kMaxPerThread;
+constexpr int kMaxRun = 8;
+constexpr int64_t kMaxNx = (int64_t)kMaxThreads * kMaxRun;
 
 unsigned long long g_launches = 0;
 
@@ -99,61 +105,108 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
 
 constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
 
-// reconstruct_left (weno.py:171-177) on the window w[0..2K] (cells in
-// increasing order for the left state, reversed for the right state).
-// Zero table entries are skipped (exact for finite windows); CHECK = true
-// turns a window with any non-finite cell into NaN as the reference's 0*inf
-// terms do -- needed only where no NaN-propagating alpha covers it.
-template <int K, bool CHECK>
-__device__ __forceinline__ double reconstruct(const double *w, int regime,
-                                              double eps, double k0_omega) {
-    if (CHECK) {
-        int bad = 0;
+// Shared-memory index of element t: one pad word per 16 elements, so that
+// the lanes of a warp walking runs of P in {1,2,4,8} consecutive cells hit
+// distinct banks.
+__device__ __forceinline__ int sk(int t) { return t + (t >> 4); }
+__host__ __device__ constexpr int sk_size(int n) { return n + (n >> 4) + 1; }
+
+// ---------------------------------------------------------------------------
+// WENO reconstruction, reference weno.py:154-177, for a run of consecutive
+// interfaces.  Notation: c_j = cell j; the left state at interface i+1/2 uses
+// the window c_{i-K..i+K}, the right state the reversed window
+// c_{i+1+K..i+1-K} (weno.py:191-199).
+//
+//   left  q_r(i) = sum_j cw[r][j] c_{i-r+j}
+//   right q_r(i) = sum_j cw[r][j] c_{i+1+r-j}
+//   left  beta_s(i) = sum_{a,b} (c_{i-s+a} S_s[a][b]) c_{i-s+b}     (a-major)
+//   right beta_r(i) = the same nine products as left beta_{K-r}(i+1),
+//                     summed in exactly the reverse order
+// (S_{K-r} is S_r flipped; checked for every table by test_abi.py), so the
+// products of the left state at i+1 are formed once and summed twice.  The
+// candidate sums follow NumPy: sequential for batches of >= 2 fields, (even
+// window slots) + (odd window slots) for a single field.
+// ---------------------------------------------------------------------------
+
+// win[0..2K] = c_{m-K..m+K} for the window centre m.
+template <int K, int REG>
+__device__ __forceinline__ double cand_left(const double *win, int r) {
+    // left q_r(m): cells m-r+j -> win[K-r+j], window slot K-r+j
+    if (REG == MGP_SUM_SEQ || K < 2) {
+        double acc = c_cw[K][r][0] * win[K - r];
 #pragma unroll
-        for (int s = 0; s <= 2 * K; ++s) bad |= !is_finite(w[s]);
-        if (bad) return __longlong_as_double(kNaNBits);
+        for (int j = 1; j <= K; ++j) acc = acc + c_cw[K][r][j] * win[K - r + j];
+        return acc;
     }
-    if (K == 0) {
-        // beta = 0, omega = raw/raw (1, or NaN when 1/eps^2 overflows)
-        return k0_omega * (c_cw[0][0][0] * w[0]);
+    double ev = 0.0, od = 0.0;
+    bool he = false, ho = false;
+#pragma unroll
+    for (int j = 0; j <= K; ++j) {
+        const int slot = K - r + j;
+        const double p = c_cw[K][r][j] * win[K - r + j];
+        if ((slot & 1) == 0) { ev = he ? ev + p : p; he = true; }
+        else { od = ho ? od + p : p; ho = true; }
     }
-    double q[K + 1], raw[K + 1];
+    return he ? (ho ? ev + od : ev) : od;
+}
+
+template <int K, int REG>
+__device__ __forceinline__ double cand_right(const double *win, int r) {
+    // right q_r(m-1): cells (m-1)+1+r-j = m+r-j -> win[K+r-j], slot K-r+j
+    if (REG == MGP_SUM_SEQ || K < 2) {
+        double acc = c_cw[K][r][0] * win[K + r];
+#pragma unroll
+        for (int j = 1; j <= K; ++j) acc = acc + c_cw[K][r][j] * win[K + r - j];
+        return acc;
+    }
+    double ev = 0.0, od = 0.0;
+    bool he = false, ho = false;
+#pragma unroll
+    for (int j = 0; j <= K; ++j) {
+        const int slot = K - r + j;
+        const double p = c_cw[K][r][j] * win[K + r - j];
+        if ((slot & 1) == 0) { ev = he ? ev + p : p; he = true; }
+        else { od = ho ? od + p : p; ho = true; }
+    }
+    return he ? (ho ? ev + od : ev) : od;
+}
+
+// Products of left beta_s(m): cells m-s+a -> win[K-s+a].  Returns the
+// forward (a-major) sum; when RIGHT, also the reverse-order sum, which is
+// right beta_{K-s}(m-1).
+template <int K, bool RIGHT>
+__device__ __forceinline__ void beta_block(const double *win, int s, double &fwd,
+                                           double &rev) {
+    constexpr int N = (K + 1) * (K + 1);
+    double p[N];
+#pragma unroll
+    for (int a = 0; a <= K; ++a)
+#pragma unroll
+        for (int b = 0; b <= K; ++b)
+            p[a * (K + 1) + b] = (win[K - s + a] * c_sm[K][s][a][b]) * win[K - s + b];
+    double f = p[0];
+#pragma unroll
+    for (int t = 1; t < N; ++t) f = f + p[t];
+    fwd = f;
+    if (RIGHT) {
+        double g = p[N - 1];
+#pragma unroll
+        for (int t = N - 2; t >= 0; --t) g = g + p[t];
+        rev = g;
+    }
+}
+
+// nonlinear weights and combination (weno.py:161-168, 176-177):
+// raw_r = d_r / ((eps+beta_r)(eps+beta_r)), S = (raw_0 + raw_1) + ...,
+// value = ((raw_0/S) q_0 + (raw_1/S) q_1) + ...  The divisions take the
+// compiler's own fast path branch-free (div_shared.cuh); if any of them was
+// outside its validity range the value is recomputed with IEEE `/`.
+template <int K>
+__device__ __forceinline__ double weno_value_ieee(const double *beta, const double *q, double eps) {
+    double raw[K + 1];
 #pragma unroll
     for (int r = 0; r <= K; ++r) {
-        const int lo = K - r;
-        double acc;
-        if (K < 2 || regime == MGP_SUM_SEQ) {
-            acc = c_cw[K][r][0] * w[lo];
-#pragma unroll
-            for (int j = 1; j <= K; ++j) acc = acc + c_cw[K][r][j] * w[lo + j];
-        } else {
-            // NumPy's contiguous einsum: (even slots) + (odd slots)
-            double ev = 0.0, od = 0.0;
-            bool he = false, ho = false;
-#pragma unroll
-            for (int j = 0; j <= K; ++j) {
-                const int s = lo + j;
-                const double p = c_cw[K][r][j] * w[s];
-                if ((s & 1) == 0) {
-                    ev = he ? ev + p : p;
-                    he = true;
-                } else {
-                    od = ho ? od + p : p;
-                    ho = true;
-                }
-            }
-            acc = he ? (ho ? ev + od : ev) : od;
-        }
-        q[r] = acc;
-        double b = 0.0;
-#pragma unroll
-        for (int i = 0; i <= K; ++i)
-#pragma unroll
-            for (int j = 0; j <= K; ++j) {
-                const double t = (w[lo + i] * c_sm[K][r][i][j]) * w[lo + j];
-                b = (i == 0 && j == 0) ? t : b + t;
-            }
-        const double e = eps + b;
+        const double e = eps + beta[r];
         raw[r] = c_d[K][r] / (e * e);
     }
     double S = raw[0];
@@ -165,124 +218,241 @@ __device__ __forceinline__ double reconstruct(const double *w, int regime,
     return v;
 }
 
+template <int K>
+__device__ __forceinline__ double weno_value(const double *beta, const double *q, double eps) {
+    bool bad = false;
+    double raw[K + 1];
+#pragma unroll
+    for (int r = 0; r <= K; ++r) {
+        const double e = eps + beta[r];
+        raw[r] = mgp::div_fast_cnum(c_d[K][r], shared_rcp(e * e), bad);
+    }
+    double S = raw[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) S = S + raw[r];
+    const SharedRcp R = shared_rcp(S);
+    double v = mgp::div_fast(raw[0], R, bad) * q[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) v = v + mgp::div_fast(raw[r], R, bad) * q[r];
+    if (bad) v = weno_value_ieee<K>(beta, q, eps);
+    return v;
+}
+
 struct Consts {
     double dt, hdt, qdt, tdt, two3, inv_dx, dx, eps, speed, half_alpha_adv;
     double k0_omega;
-    bool dx_pow2;
+    int dx_pow2;
 };
 
-// Field: the shared-memory image of one field plus the per-stage machinery.
-template <int K, int MODEL>
+// One field in shared memory; thread `run` owns interfaces and cells
+// [run*P, run*P + P) of the periodic mesh.
+template <int K, int REG, int MODEL, int P>
 struct Field {
-    static constexpr int H = K + 1;   // periodic halo on each side
-    int nx;
-    double *s_u;    // [nx + 2H]  stage input, cell c at s_u[c + H]
-    double *s_u0;   // [nx]       RK base state
-    double *s_L;    // [nx]       left states, then the interface flux
-    double *s_R;    // [nx]       right states
-    unsigned long long *s_red;  // [32]
-    double *s_sum;  // [3 * 32]
+    static constexpr int H = K + 1;  // periodic halo cells on each side
+    int nx, run, i0;
+    double *s_u;   // stage input, cell c at s_u[sk(c + H)], c in [-H, nx + H)
+    double *s_L;   // left states, then interface fluxes, at s_L[sk(i)]
+    double *s_R;   // right states, then results, at s_R[sk(i)]
+    unsigned long long *s_red;
+    double u0[P];  // RK base of the owned cells
 
+    __device__ __forceinline__ double cell(int c) const { return s_u[sk(c + H)]; }
     __device__ __forceinline__ void put(int c, double v) {
-        s_u[c + H] = v;
-        if (c < H) s_u[nx + H + c] = v;
-        if (c >= nx - H) s_u[c - (nx - H)] = v;
+        s_u[sk(c + H)] = v;
+        if (c < H) s_u[sk(nx + H + c)] = v;
+        if (c >= nx - H) s_u[sk(c - (nx - H))] = v;
     }
-    __device__ __forceinline__ double get(int c) const { return s_u[c + H]; }
 
-    // A = SemiDiscreteOperator.rhs(s_u), written to s_R[c] for the cells this
-    // thread owns (c = tid + j*blockDim.x; the thread that reconstructs
-    // interface c+1/2 is the one that owns cell c, so s_R[c] is free to
-    // reuse once the flux is formed).  Starts with a barrier (s_u must be
-    // complete) and ends after the flux barrier; s_u is not modified.
-    __device__ void rhs(const Consts &k, int regime) {
-        const int tid = threadIdx.x, nt = blockDim.x;
-        __syncthreads();
+    // Left/right interface states of the owned run -> s_L, s_R; returns the
+    // bits of this thread's NaN-propagating max |u| (Burgers).
+    __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
         unsigned long long m = 0;
+        const int n = (nx - i0 < P) ? nx - i0 : P;
+        if (n <= 0) return 0;
+        constexpr bool kCheck = (MODEL == MGP_MODEL_ADVECTION);
+        if (K == 0) {
+            // beta = 0, omega = raw/raw (1, or NaN when 1/eps^2 overflows)
+            double c0 = cell(i0);
 #pragma unroll 1
-        for (int i = tid; i < nx; i += nt) {
-            const double *c = s_u + H + i;
-            double w[2 * K + 2];
+            for (int p = 0; p < n; ++p) {
+                const int i = i0 + p;
+                const double c1 = cell(i + 1);
+                double ul = k.k0_omega * (c_cw[0][0][0] * c0);
+                double ur = k.k0_omega * (c_cw[0][0][0] * c1);
+                if (kCheck) {
+                    if (!is_finite(c0)) ul = __longlong_as_double(kNaNBits);
+                    if (!is_finite(c1)) ur = __longlong_as_double(kNaNBits);
+                }
+                s_L[sk(i)] = ul;
+                s_R[sk(i)] = ur;
+                if (MODEL == MGP_MODEL_BURGERS) {
+                    m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
+                    if (!is_finite(c0)) m = kNaNBits;
+                }
+                c0 = c1;
+            }
+            return m;
+        }
+        double win[2 * K + 1];
 #pragma unroll
-            for (int s = 0; s < 2 * K + 2; ++s) w[s] = c[s - K];
-            double wr[2 * K + 1];
+        for (int t = 0; t <= 2 * K; ++t) win[t] = cell(i0 - K + t);
+        // warm-up: left state data of the first interface
+        double bl[K + 1], ql[K + 1];
 #pragma unroll
-            for (int s = 0; s <= 2 * K; ++s) wr[s] = w[2 * K + 1 - s];
-            constexpr bool kCheck = (MODEL == MGP_MODEL_ADVECTION);
-            const double ul = reconstruct<K, kCheck>(w, regime, k.eps, k.k0_omega);
-            const double ur = reconstruct<K, kCheck>(wr, regime, k.eps, k.k0_omega);
-            s_L[i] = ul;
-            s_R[i] = ur;
+        for (int s = 0; s <= K; ++s) {
+            double dummy;
+            beta_block<K, false>(win, s, bl[s], dummy);
+        }
+#pragma unroll
+        for (int r = 0; r <= K; ++r) ql[r] = cand_left<K, REG>(win, r);
+#pragma unroll 1
+        for (int p = 0; p < n; ++p) {
+            const int i = i0 + p;
+            // window of the left state at i+1; the nonfinite flag covers the
+            // left window of interface i (Burgers: any non-finite cell makes
+            // the reference's alpha NaN)
+            const bool bad_here = !is_finite(win[K]);
+            bool bad_left = false;
+            if (kCheck) {
+#pragma unroll
+                for (int t = 0; t <= 2 * K; ++t) bad_left |= !is_finite(win[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
+            win[2 * K] = cell(i + 1 + K);
+            bool bad_right = false;
+            if (kCheck) {
+#pragma unroll
+                for (int t = 0; t <= 2 * K; ++t) bad_right |= !is_finite(win[t]);
+            }
+            double bl_next[K + 1], br[K + 1], ql_next[K + 1], qr[K + 1];
+#pragma unroll
+            for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl_next[s], br[K - s]);
+#pragma unroll
+            for (int r = 0; r <= K; ++r) {
+                ql_next[r] = cand_left<K, REG>(win, r);
+                qr[r] = cand_right<K, REG>(win, r);
+            }
+            double ul = weno_value<K>(bl, ql, k.eps);
+            double ur = weno_value<K>(br, qr, k.eps);
+            if (kCheck) {
+                if (bad_left) ul = __longlong_as_double(kNaNBits);
+                if (bad_right) ur = __longlong_as_double(kNaNBits);
+            }
+            s_L[sk(i)] = ul;
+            s_R[sk(i)] = ur;
             if (MODEL == MGP_MODEL_BURGERS) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
-                // a non-finite cell makes every window holding it NaN in the
-                // reference, hence alpha NaN (np.max propagates it)
-                if (!is_finite(w[K])) m = kNaNBits;
+                if (bad_here) m = kNaNBits;
+            }
+#pragma unroll
+            for (int s = 0; s <= K; ++s) {
+                bl[s] = bl_next[s];
+                ql[s] = ql_next[s];
             }
         }
+        return m;
+    }
+
+    // A = SemiDiscreteOperator.rhs(s_u) for the owned cells (flux.py:70-88,
+    // 159-161).  Precondition: s_u complete (caller synchronised).  On
+    // return A[] holds the owned cells' rhs; s_u is unchanged.
+    __device__ __forceinline__ void rhs(const Consts &k, double *A) {
+        unsigned long long m = reconstruct(k);
         double half_alpha;
         if (MODEL == MGP_MODEL_BURGERS) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
                 m = umax64(m, __shfl_xor_sync(0xffffffffu, m, o));
+            const int tid = threadIdx.x;
             if ((tid & 31) == 0) s_red[tid >> 5] = m;
             __syncthreads();
             m = s_red[0];
-            const int nw = (nt + 31) >> 5;
+            const int nw = (blockDim.x + 31) >> 5;
             for (int w = 1; w < nw; ++w) m = umax64(m, s_red[w]);
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         } else {
             half_alpha = k.half_alpha_adv;
         }
-#pragma unroll 1
-        for (int i = tid; i < nx; i += nt) {
-            const double ul = s_L[i], ur = s_R[i];
-            double fl, fr;
-            if (MODEL == MGP_MODEL_BURGERS) {
-                fl = (0.5 * ul) * ul;
-                fr = (0.5 * ur) * ur;
-            } else {
-                fl = k.speed * ul;
-                fr = k.speed * ur;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int i = i0 + p;
+            if (i < nx) {
+                const double ul = s_L[sk(i)], ur = s_R[sk(i)];
+                double fl, fr;
+                if (MODEL == MGP_MODEL_BURGERS) {
+                    fl = (0.5 * ul) * ul;
+                    fr = (0.5 * ur) * ur;
+                } else {
+                    fl = k.speed * ul;
+                    fr = k.speed * ur;
+                }
+                s_L[sk(i)] = (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
             }
-            s_L[i] = (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
         }
         __syncthreads();
-#pragma unroll 1
-        for (int c = tid; c < nx; c += nt) {
-            const double fm = s_L[c == 0 ? nx - 1 : c - 1];
-            const double neg = -(s_L[c] - fm);
-            s_R[c] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+            const int c = i0 + p;
+            if (c < nx) {
+                const double fm = s_L[sk(c == 0 ? nx - 1 : c - 1)];
+                const double neg = -(s_L[sk(c)] - fm);
+                A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+            }
         }
     }
 
-    // RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned cells,
-    // result in s_R[c]; rk_order 0 gives the rhs.  s_u keeps the last stage
-    // input (the caller commits the result with put()).
-    __device__ void phi(const Consts &k, int rk, int regime) {
-        const int tid = threadIdx.x, nt = blockDim.x;
-        for (int c = tid; c < nx; c += nt) s_u0[c] = get(c);
-        rhs(k, regime);
-        if (rk == 0) return;
-        for (int c = tid; c < nx; c += nt) {
-            const double u1 = s_u0[c] + k.dt * s_R[c];
-            s_R[c] = u1;
-            if (rk > 1) put(c, u1);
-        }
-        if (rk == 1) return;
-        rhs(k, regime);
-        if (rk == 2) {
-            for (int c = tid; c < nx; c += nt)
-                s_R[c] = ((0.5 * s_u0[c]) + (0.5 * get(c))) + (k.hdt * s_R[c]);
+    // res = RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned
+    // cells, written to s_R[sk(c)]; rk_order 0 gives the rhs.  Precondition:
+    // s_u complete and synchronised.  Leaves s_u holding the last stage input.
+    __device__ __forceinline__ void phi(const Consts &k, int rk) {
+        double A[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (i0 + p < nx) u0[p] = cell(i0 + p);
+        rhs(k, A);
+        if (rk == 0) {
+            store_res(A);
             return;
         }
-        for (int c = tid; c < nx; c += nt) {
-            const double u2 = ((0.75 * s_u0[c]) + (0.25 * get(c))) + (k.qdt * s_R[c]);
-            put(c, u2);
+        double st[P];
+#pragma unroll
+        for (int p = 0; p < P; ++p) st[p] = u0[p] + k.dt * A[p];
+        if (rk == 1) {
+            store_res(st);
+            return;
         }
-        rhs(k, regime);
-        for (int c = tid; c < nx; c += nt)
-            s_R[c] = ((s_u0[c] / 3.0) + (k.two3 * get(c))) + (k.tdt * s_R[c]);
+        commit(st);
+        __syncthreads();
+        rhs(k, A);
+        if (rk == 2) {
+#pragma unroll
+            for (int p = 0; p < P; ++p)
+                st[p] = ((0.5 * u0[p]) + (0.5 * st[p])) + (k.hdt * A[p]);
+            store_res(st);
+            return;
+        }
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            st[p] = ((0.75 * u0[p]) + (0.25 * st[p])) + (k.qdt * A[p]);
+        commit(st);
+        __syncthreads();
+        rhs(k, A);
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            st[p] = ((u0[p] / 3.0) + (k.two3 * st[p])) + (k.tdt * A[p]);
+        store_res(st);
+    }
+
+    __device__ __forceinline__ void commit(const double *v) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (i0 + p < nx) put(i0 + p, v[p]);
+    }
+    __device__ __forceinline__ void store_res(const double *v) {
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            if (i0 + p < nx) s_R[sk(i0 + p)] = v[p];
     }
 };
 
@@ -296,23 +466,23 @@ __device__ __forceinline__ double g_value(int mode, const double *g, int c) {
     return mode == MGP_G_ARRAY ? g[c] : 0.0;
 }
 
-template <int K, int MODEL>
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    sweep_kernel(const mgp_sweep_args a, const Consts k) {
+template <int K, int REG, int MODEL, int P, int REGS>
+__global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
     extern __shared__ double smem[];
-    using F = Field<K, MODEL>;
+    using F = Field<K, REG, MODEL, P>;
     F f;
     const int nx = (int)a.phi.nx;
-    f.nx = nx;
-    f.s_u = smem;
-    f.s_u0 = f.s_u + nx + 2 * F::H;
-    f.s_L = f.s_u0 + nx;
-    f.s_R = f.s_L + nx;
-    f.s_sum = f.s_R + nx;
-    f.s_red = reinterpret_cast<unsigned long long *>(f.s_sum + 3 * 32);
-
     const int tid = threadIdx.x, nt = blockDim.x;
+    f.nx = nx;
+    f.run = tid;
+    f.i0 = tid * P;
+    f.s_u = smem;
+    f.s_L = f.s_u + sk_size(nx + 2 * F::H);
+    f.s_R = f.s_L + sk_size(nx);
+    double *s_sum = f.s_R + sk_size(nx);
+    f.s_red = reinterpret_cast<unsigned long long *>(s_sum + 3 * 32);
     const int rk = a.phi.rk_order;
+    const int total = a.n_steps + (a.tail != MGP_TAIL_NONE ? 1 : 0);
 
     for (int64_t b = blockIdx.x; b < a.n_chunks; b += gridDim.x) {
         double acc_r = 0.0, acc_e = 0.0, acc_n = 0.0;
@@ -327,29 +497,31 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             }
             if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
         }
-        for (int s = 1; s <= a.n_steps; ++s) {
-            f.phi(k, rk, a.phi.regime);
-            const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
-            double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
-            const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
-            for (int c = tid; c < nx; c += nt) {
-                const double v = add_g(f.s_R[c], a.g_mode, g, c);
-                f.put(c, v);
-                if (st) st[c] = v;
-                if (rs) {
-                    const double d = v - rs[c];
-                    acc_e = acc_e + d * d;
+        for (int s = 1; s <= total; ++s) {
+            __syncthreads();  // s_u complete
+            f.phi(k, rk);
+            __syncthreads();  // results in s_R complete
+            if (s <= a.n_steps) {
+                const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
+                double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
+                const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
+                for (int c = tid; c < nx; c += nt) {
+                    const double v = add_g(f.s_R[sk(c)], a.g_mode, g, c);
+                    f.put(c, v);
+                    if (st) st[c] = v;
+                    if (rs) {
+                        const double d = v - rs[c];
+                        acc_e = acc_e + d * d;
+                    }
+                    if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
                 }
-                if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
+                continue;
             }
-        }
-        if (a.tail != MGP_TAIL_NONE) {
-            f.phi(k, rk, a.tail_regime);
             const double *tg = a.tail_g ? a.tail_g + b * a.tg_s : nullptr;
             if (a.tail == MGP_TAIL_PHI) {
                 double *out = a.tail_out + b * a.to_s;
                 for (int c = tid; c < nx; c += nt)
-                    out[c] = add_g(f.s_R[c], a.tail_g_mode, tg, c);
+                    out[c] = add_g(f.s_R[sk(c)], a.tail_g_mode, tg, c);
             } else if (a.tail == MGP_TAIL_RESTRICT) {
                 // mgrit.py:211-215: g_c = (g_f + phi) - psi;
                 // u_c = phi + g_f (last-step) or u_f (injection)
@@ -358,22 +530,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
                 double *gc = a.tail_out + b * a.to_s;
                 double *uc = a.tail_out2 + b * a.to2_s;
                 for (int c = tid; c < nx; c += nt) {
-                    const double gf = g_value(a.tail_g_mode, tg, c);
                     const double p = phi[c];
-                    const double left = (a.tail_g_mode == MGP_G_NONE) ? p : gf + p;
-                    gc[c] = left - f.s_R[c];
-                    uc[c] = (a.guess == MGP_GUESS_LAST_STEP)
-                                ? add_g(p, a.tail_g_mode, tg, c)
-                                : uf[c];
+                    const double left =
+                        (a.tail_g_mode == MGP_G_NONE) ? p : g_value(a.tail_g_mode, tg, c) + p;
+                    gc[c] = left - f.s_R[sk(c)];
+                    uc[c] = (a.guess == MGP_GUESS_LAST_STEP) ? add_g(p, a.tail_g_mode, tg, c)
+                                                             : uf[c];
                 }
             } else {  // MGP_TAIL_RESID, mgrit.py:268: (g + Phi(u_prev)) - u
                 const double *tgt = a.aux + b * a.aux_s;
                 const bool last = (b == a.n_chunks - 1) && a.ref_last_next;
                 const double *rn = (last && a.ref) ? a.ref + (b + 1) * a.ref_cs : nullptr;
                 for (int c = tid; c < nx; c += nt) {
-                    const double pred = (a.tail_g_mode == MGP_G_NONE)
-                                            ? f.s_R[c]
-                                            : g_value(a.tail_g_mode, tg, c) + f.s_R[c];
+                    const double y = f.s_R[sk(c)];
+                    const double pred =
+                        (a.tail_g_mode == MGP_G_NONE) ? y : g_value(a.tail_g_mode, tg, c) + y;
                     const double u = tgt[c];
                     const double r = pred - u;
                     acc_r = acc_r + r * r;
@@ -397,19 +568,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
             }
             __syncthreads();
             if ((tid & 31) == 0) {
-                f.s_sum[3 * (tid >> 5) + 0] = acc_r;
-                f.s_sum[3 * (tid >> 5) + 1] = acc_e;
-                f.s_sum[3 * (tid >> 5) + 2] = acc_n;
+                s_sum[3 * (tid >> 5) + 0] = acc_r;
+                s_sum[3 * (tid >> 5) + 1] = acc_e;
+                s_sum[3 * (tid >> 5) + 2] = acc_n;
             }
             __syncthreads();
             if (tid < 3) {
                 double t = 0.0;
                 const int nw = (nt + 31) >> 5;
-                for (int w = 0; w < nw; ++w) t = t + f.s_sum[3 * w + tid];
+                for (int w = 0; w < nw; ++w) t = t + s_sum[3 * w + tid];
                 a.partials[3 * b + tid] = t;
             }
         }
-        __syncthreads();  // s_u / s_sum reuse by the next chunk
+        __syncthreads();  // shared buffers are reused by the next chunk
     }
 }
 
@@ -460,24 +631,43 @@ Consts make_consts(const mgp_phi &p) {
     return k;
 }
 
-int threads_for(int64_t nx) {
-    int64_t nt = (nx + kMaxPerThread - 1) / kMaxPerThread;
-    if (nt < 128) nt = nx < 128 ? nx : 128;  // keep >= 4 warps when possible
+// Cells per thread run.  Single-field launches (the sequential coarse solve)
+// use the most threads (shortest per-step latency); batched launches use
+// longer runs, which share more reconstruction products per interface.
+int run_length(int64_t nx, int64_t n_chunks) {
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("MGP_RUN");
+        env = e ? atoi(e) : 0;
+    }
+    int p = 1;
+    while ((nx + p - 1) / p > kMaxThreads) p *= 2;
+    if (n_chunks > 1) {
+        const int want = env > 0 ? env : (nx >= 1024 ? 8 : 4);
+        while (p < want && p < kMaxRun) p *= 2;
+    } else if (env > 0 && n_chunks == 1) {
+        // keep the latency-oriented choice for single fields
+    }
+    return p;
+}
+
+int threads_for(int64_t nx, int p) {
+    int64_t nt = (nx + p - 1) / p;
     nt = (nt + 31) / 32 * 32;
-    if (nt > kMaxThreads) nt = kMaxThreads;
     return (int)nt;
 }
 
 size_t smem_bytes(int64_t nx, int k) {
-    return sizeof(double) * (size_t)(nx + 2 * (k + 1) + 3 * nx + 3 * 32) +
+    const int H = k + 1;
+    return sizeof(double) * (size_t)(sk_size((int)nx + 2 * H) + 2 * sk_size((int)nx) + 3 * 32) +
            sizeof(unsigned long long) * 32;
 }
 
-template <int K, int MODEL>
+template <int K, int REG, int MODEL, int P, int REGS>
 int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
-    const int nt = threads_for(a.phi.nx);
+    const int nt = threads_for(a.phi.nx, P);
     const size_t sm = smem_bytes(a.phi.nx, K);
-    auto kern = sweep_kernel<K, MODEL>;
+    auto kern = sweep_kernel<K, REG, MODEL, P, REGS>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -493,13 +683,34 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
+template <int K, int REG, int MODEL, int P>
+int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_t<K, REG, MODEL, P, 128>(a, st);
+}
+
+template <int K, int REG, int MODEL>
+int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
+    switch (run_length(a.phi.nx, a.n_chunks)) {
+        case 1: return launch_r<K, REG, MODEL, 1>(a, st);
+        case 2: return launch_r<K, REG, MODEL, 2>(a, st);
+        case 4: return launch_r<K, REG, MODEL, 4>(a, st);
+        case 8: return launch_r<K, REG, MODEL, 8>(a, st);
+    }
+    return MGP_EINVAL;
+}
+
 template <int MODEL>
 int launch_m(const mgp_sweep_args &a, cudaStream_t st) {
+    const int reg = a.n_steps > 0 ? a.phi.regime : a.tail_regime;
     switch (a.phi.weno_k) {
-        case 0: return launch_t<0, MODEL>(a, st);
-        case 1: return launch_t<1, MODEL>(a, st);
-        case 2: return launch_t<2, MODEL>(a, st);
-        case 3: return launch_t<3, MODEL>(a, st);
+        case 0: return launch_p<0, MGP_SUM_SEQ, MODEL>(a, st);
+        case 1: return launch_p<1, MGP_SUM_SEQ, MODEL>(a, st);
+        case 2:
+            return reg == MGP_SUM_SEQ ? launch_p<2, MGP_SUM_SEQ, MODEL>(a, st)
+                                      : launch_p<2, MGP_SUM_LANE2, MODEL>(a, st);
+        case 3:
+            return reg == MGP_SUM_SEQ ? launch_p<3, MGP_SUM_SEQ, MODEL>(a, st)
+                                      : launch_p<3, MGP_SUM_LANE2, MODEL>(a, st);
     }
     return MGP_EINVAL;
 }
@@ -529,6 +740,9 @@ int validate(const mgp_sweep_args *a) {
         if (a->guess != MGP_GUESS_INJECTION && a->guess != MGP_GUESS_LAST_STEP) return MGP_EINVAL;
     }
     if (a->tail == MGP_TAIL_RESID && (!a->aux || !a->partials)) return MGP_EINVAL;
+    // one summation regime per launch (the kernel is specialised on it)
+    if (a->n_steps > 0 && a->tail != MGP_TAIL_NONE && a->tail_regime != p.regime)
+        return MGP_EINVAL;
     return MGP_OK;
 }
 

@@ -94,9 +94,9 @@ def _pair(n_x=32, n_t=64, m=4, L=3, k=2, rk=3, cfl=0.2, seed=7):
 def _same(gpu, cpu):
     for l, lv in enumerate(cpu.levels):
         got = gpu.levels[l].u.cpu().numpy()
-        assert np.array_equal(got, lv.u), l
+        assert np.array_equal(got, lv.u, equal_nan=True), l
         if l > 0:
-            assert np.array_equal(gpu.levels[l].g.cpu().numpy(), lv.g), l
+            assert np.array_equal(gpu.levels[l].g.cpu().numpy(), lv.g, equal_nan=True), l
 
 
 SEQUENCES = [
@@ -113,7 +113,8 @@ def test_level_operations_in_any_order(seq):
     gpu, cpu = _pair()
     for op in seq:
         if op == "res":
-            assert abs(gpu.residual_norm() - cpu.residual_norm()) <= RTOL * cpu.residual_norm()
+            rg, rc = gpu.residual_norm(), cpu.residual_norm()
+            assert (np.isnan(rg) and np.isnan(rc)) or abs(rg - rc) <= RTOL * abs(rc)
             continue
         kind, l = op[0], op[1:]
         if op == "cs":
