@@ -253,8 +253,8 @@ struct Field {
     double *s_u;   // stage input, cell c at s_u[sk(c + H)], c in [-H, nx + H)
     double *s_L;   // left states, then interface fluxes, at s_L[sk(i)]
     double *s_R;   // right states, then results, at s_R[sk(i)]
+    double *s_u0;  // RK base state of the cells, at s_u0[sk(c)]
     unsigned long long *s_red;
-    double u0[P];  // RK base of the owned cells
 
     __device__ __forceinline__ double cell(int c) const { return s_u[sk(c + H)]; }
     __device__ __forceinline__ void put(int c, double v) {
@@ -405,43 +405,44 @@ struct Field {
     // res = RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned
     // cells, written to s_R[sk(c)]; rk_order 0 gives the rhs.  Precondition:
     // s_u complete and synchronised.  Leaves s_u holding the last stage input.
+    // The RK base and the stage values live in shared memory (s_u0, s_u), so
+    // no per-cell state is held in registers across the reconstruction.
+    __device__ __forceinline__ double u0(int p) const { return s_u0[sk(i0 + p)]; }
+
     __device__ __forceinline__ void phi(const Consts &k, int rk) {
-        double A[P];
 #pragma unroll
         for (int p = 0; p < P; ++p)
-            if (i0 + p < nx) u0[p] = cell(i0 + p);
-        rhs(k, A);
-        if (rk == 0) {
-            store_res(A);
-            return;
+            if (i0 + p < nx) s_u0[sk(i0 + p)] = cell(i0 + p);
+        const int stages = rk == 0 ? 1 : rk;
+        // one call site of the reconstruction for every stage (code size)
+#pragma unroll 1
+        for (int sg = 0; sg < stages; ++sg) {
+            if (sg > 0) __syncthreads();  // committed stage values visible
+            double A[P];
+            rhs(k, A);
+            double st[P];
+            const bool last = (sg == stages - 1);
+#pragma unroll
+            for (int p = 0; p < P; ++p) {
+                if (rk == 0) {
+                    st[p] = A[p];
+                } else if (sg == 0) {
+                    st[p] = u0(p) + k.dt * A[p];
+                } else if (rk == 2) {
+                    st[p] = ((0.5 * u0(p)) + (0.5 * stage(p))) + (k.hdt * A[p]);
+                } else if (sg == 1) {
+                    st[p] = ((0.75 * u0(p)) + (0.25 * stage(p))) + (k.qdt * A[p]);
+                } else {
+                    st[p] = ((u0(p) / 3.0) + (k.two3 * stage(p))) + (k.tdt * A[p]);
+                }
+            }
+            if (last) store_res(st);
+            else commit(st);
         }
-        double st[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) st[p] = u0[p] + k.dt * A[p];
-        if (rk == 1) {
-            store_res(st);
-            return;
-        }
-        commit(st);
-        __syncthreads();
-        rhs(k, A);
-        if (rk == 2) {
-#pragma unroll
-            for (int p = 0; p < P; ++p)
-                st[p] = ((0.5 * u0[p]) + (0.5 * st[p])) + (k.hdt * A[p]);
-            store_res(st);
-            return;
-        }
-#pragma unroll
-        for (int p = 0; p < P; ++p)
-            st[p] = ((0.75 * u0[p]) + (0.25 * st[p])) + (k.qdt * A[p]);
-        commit(st);
-        __syncthreads();
-        rhs(k, A);
-#pragma unroll
-        for (int p = 0; p < P; ++p)
-            st[p] = ((u0[p] / 3.0) + (k.two3 * st[p])) + (k.tdt * A[p]);
-        store_res(st);
+    }
+
+    __device__ __forceinline__ double stage(int p) const {
+        return (i0 + p < nx) ? cell(i0 + p) : 0.0;
     }
 
     __device__ __forceinline__ void commit(const double *v) {
@@ -479,7 +480,8 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     f.s_u = smem;
     f.s_L = f.s_u + sk_size(nx + 2 * F::H);
     f.s_R = f.s_L + sk_size(nx);
-    double *s_sum = f.s_R + sk_size(nx);
+    f.s_u0 = f.s_R + sk_size(nx);
+    double *s_sum = f.s_u0 + sk_size(nx);
     f.s_red = reinterpret_cast<unsigned long long *>(s_sum + 3 * 32);
     const int rk = a.phi.rk_order;
     const int total = a.n_steps + (a.tail != MGP_TAIL_NONE ? 1 : 0);
@@ -659,7 +661,7 @@ int threads_for(int64_t nx, int p) {
 
 size_t smem_bytes(int64_t nx, int k) {
     const int H = k + 1;
-    return sizeof(double) * (size_t)(sk_size((int)nx + 2 * H) + 2 * sk_size((int)nx) + 3 * 32) +
+    return sizeof(double) * (size_t)(sk_size((int)nx + 2 * H) + 3 * sk_size((int)nx) + 3 * 32) +
            sizeof(unsigned long long) * 32;
 }
 
@@ -683,9 +685,30 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
+#ifndef MGP_REGS
+#define MGP_REGS 128
+#endif
+
 template <int K, int REG, int MODEL, int P>
 int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
-    return launch_t<K, REG, MODEL, P, 128>(a, st);
+#ifdef MGP_EXPERIMENT
+    // register-budget experiments (tools/): MGP_MAXREG selects the variant
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("MGP_MAXREG");
+        env = e ? atoi(e) : 0;
+    }
+    if (K == 2 && MODEL == MGP_MODEL_BURGERS && P >= 4) {
+        switch (env) {
+            case 80: return launch_t<K, REG, MODEL, P, 80>(a, st);
+            case 96: return launch_t<K, REG, MODEL, P, 96>(a, st);
+            case 104: return launch_t<K, REG, MODEL, P, 104>(a, st);
+            case 112: return launch_t<K, REG, MODEL, P, 112>(a, st);
+            default: break;
+        }
+    }
+#endif
+    return launch_t<K, REG, MODEL, P, MGP_REGS>(a, st);
 }
 
 template <int K, int REG, int MODEL>
