@@ -362,7 +362,8 @@ def run_ours(args):
         "flops_per_point_update": flops_pt,
         "kernel_share_of_step": kernel_ms / step_total_ms if step_total_ms else None,
         "traffic": prof.get("dram_bytes_per_launch"),
-        "algorithmic_bytes_per_launch": 16 * pb.m * nc * pb.n_x,
+        "algorithmic_bytes_per_launch": {"fused_f_c": 16 * nc * pb.n_x,
+                                         "f_store": 8 * pb.m * nc * pb.n_x},
     }
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
