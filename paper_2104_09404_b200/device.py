@@ -17,8 +17,31 @@ from ._lib import (G_NONE, MgpPhi, MgpSweepArgs, SUM_LANE2, SUM_SEQ,
 
 DTYPE = torch.float64
 
+# Host-logic test hook.  Tests that exercise the hierarchy / distributed
+# bookkeeping on a CPU-only machine install an emulator of mgp_sweep
+# (tests/sweep_emulator.py, built on the oracle) together with the torch
+# device it works on.  Nothing in the package installs one: without it every
+# call goes to libmgrit_phi.so and a missing GPU raises.
+_emulator = None
+
+
+def install_emulator(sweep_fn, sum_fn, dev: str = "cpu") -> None:
+    global _emulator
+    _emulator = (sweep_fn, sum_fn, torch.device(dev))
+
+
+def remove_emulator() -> None:
+    global _emulator
+    _emulator = None
+
+
+def emulated() -> bool:
+    return _emulator is not None
+
 
 def device() -> torch.device:
+    if _emulator is not None:
+        return _emulator[2]
     if not torch.cuda.is_available():
         raise RuntimeError("the B200 MGRIT path needs a CUDA device "
                            "(there is no CPU fallback)")
@@ -61,6 +84,10 @@ def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
           to2_s: int = 0, aux=None, aux_s: int = 0, aux2=None, aux2_s: int = 0,
           ref=None, ref_cs: int = 0, ref_ss: int = 0, ref_last_next: int = 0,
           count_nonfinite: int = 0, partials=None, what: str = "mgp_sweep"):
+    if _emulator is not None:
+        kw = dict(locals())
+        kw.pop("phi")
+        return _emulator[0](phi, **kw)
     a = MgpSweepArgs()
     a.phi = phi
     a.n_chunks = int(n_chunks)
@@ -84,6 +111,8 @@ def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
 
 
 def sum_partials(partials: torch.Tensor, n: int, width: int, out: torch.Tensor):
+    if _emulator is not None:
+        return _emulator[1](partials, n, width, out)
     rc = _lib.load().mgp_sum_partials(ptr(partials), int(n), int(width), ptr(out),
                                       ctypes.c_void_p(stream_handle()))
     _lib.check(rc, "mgp_sum_partials")

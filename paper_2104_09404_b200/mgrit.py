@@ -166,7 +166,7 @@ class MgritHierarchy:
             raise DimensionError(f"initial state must be (1, N), got {tuple(u0.shape)}")
         self.nx = nx = u0.shape[1]
         self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
-        if nx > dev._lib.max_nx():
+        if not dev.emulated() and nx > dev._lib.max_nx():
             raise ConfigError(f"N_x = {nx} exceeds the single-CTA field limit "
                               f"{dev._lib.max_nx()} of this build")
         self._u0 = u0[0].contiguous()

@@ -70,7 +70,8 @@ def solve_serial(stepper, initial_state, time_grid: TemporalGrid,
             per_node = torch.where(torch.isnan(per_node), torch.zeros_like(per_node),
                                    per_node)
             max_speed = float(per_node.max().item())
-    torch.cuda.synchronize()
+    if values.is_cuda:
+        torch.cuda.synchronize()
     wall = time.perf_counter() - start
     trajectory = Trajectory(time_grid, space_grid, values.cpu().numpy())
     cfl = max_speed * time_grid.dt / space_grid.dx

@@ -1,0 +1,80 @@
+"""CPU: the hierarchy's host bookkeeping (C-points-only finest storage,
+lazy F-points, ping-pong buffers, level views, monitor paths) driven through
+the mgp_sweep emulator (tests/sweep_emulator.py) equals the oracle
+restatement of the reference hierarchy.  The kernels themselves are checked
+on the GPU (test_gpu_*)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_09404_b200 as P
+from oracle import mgrit_oracle
+
+import sweep_emulator
+
+
+@pytest.fixture(autouse=True)
+def emulator():
+    sweep_emulator.install()
+    yield
+    sweep_emulator.remove()
+
+
+def _pair(n_x=16, n_t=32, m=2, L=3, k=1, rk=2, cfl=0.2, seed=5, relaxation="fcf"):
+    pb = P.Problem(name="ops", n_x=n_x, n_t=n_t, cfl=cfl, n_modes=2, seed=seed,
+                   weno_order=(2 * k + 1,), stepper=({1: "fe", 2: "ssprk2", 3: "ssprk3"}[rk],),
+                   n_levels=L, m=m, relaxation=relaxation)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    h = P.MgritHierarchy(pb.steppers(tg), u0, tg, pb.space_grid(), pb.options())
+    ost = [oracle.OracleStepper(k=k, rk_order=rk, dt=tg.dt * m ** l, dx=1.0 / n_x, nthreads=1)
+           for l in range(L)]
+    o = mgrit_oracle.Hierarchy(ost, u0, n_t, tg.dt,
+                               mgrit_oracle.Options(n_levels=L, m=m, relaxation=relaxation))
+    return h, o, pb, u0, tg
+
+
+@pytest.mark.parametrize("seq", [
+    ["f0", "c0", "f0", "r0", "f1", "c1", "r1", "cs", "i1", "i0"],
+    ["c0", "c0", "f0", "c0", "r0"],
+    ["f0", "c0", "c0", "r0", "cs", "i0"],
+    ["r0", "r1", "cs", "i1", "i0"],
+])
+def test_level_ops_match_oracle(seq):
+    h, o, *_ = _pair()
+    for op in seq + ["res"]:
+        if op == "res":
+            np.testing.assert_allclose(h.residual_norm(), o.residual_norm(), rtol=1e-12)
+            continue
+        if op == "cs":
+            h.coarse_solve(); o.coarse_solve()
+        else:
+            getattr(h, {"f": "f_relax", "c": "c_relax", "r": "restrict",
+                        "i": "interpolate"}[op[0]])(int(op[1:]))
+            getattr(o, {"f": "f_relax", "c": "c_relax", "r": "restrict",
+                        "i": "interpolate"}[op[0]])(int(op[1:]))
+        for l in range(3):
+            assert np.array_equal(h.levels[l].u.numpy(), o.levels[l].u), (op, l)
+
+
+@pytest.mark.parametrize("cycle,relax,guess", [("v", "fcf", "last-step"), ("f", "f", "injection")])
+def test_solve_matches_oracle(cycle, relax, guess):
+    pb = P.Problem(name="s", n_x=16, n_t=32, cfl=0.1, n_modes=2, weno_order=(3,),
+                   stepper=("ssprk2",), n_levels=3, m=2, cycle=cycle, relaxation=relax,
+                   guess=guess, max_iters=4)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    ref = P.serial.march(steppers[0], u0, pb.n_t)
+    traj, rec = P.mgrit_solve(steppers, u0, tg, pb.space_grid(), pb.options(), reference=ref)
+    ost = [oracle.OracleStepper(k=1, rk_order=2, dt=tg.dt * 2 ** l, dx=1 / 16, nthreads=1)
+           for l in range(3)]
+    oref = mgrit_oracle.march(ost[0], u0, pb.n_t)
+    assert np.array_equal(ref.numpy(), oref)
+    otraj, orec = mgrit_oracle.mgrit_solve(
+        ost, u0, pb.n_t, tg.dt, mgrit_oracle.Options(n_levels=3, m=2, cycle=cycle,
+                                                     relaxation=relax, guess=guess,
+                                                     max_iters=4), reference=oref)
+    assert np.array_equal(traj.values, otraj)
+    np.testing.assert_allclose(rec.residuals, orec.residuals, rtol=1e-12)
+    np.testing.assert_allclose(rec.errors, orec.errors, rtol=1e-12)
