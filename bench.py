@@ -232,26 +232,40 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pb = workload(args.workload)
     u0 = pb.initial_state()
-    tg = pb.time_grid(u0)
+    tg1 = pb.time_grid(u0)
     sg = pb.space_grid()
-    steppers = pb.steppers(tg)
-    units = relax_units(pb)
+    units = relax_units(pb)              # per rank (weak scaling: fixed per-GPU work)
     k = (pb.weno_order[0] - 1) // 2
     rk = {"fe": 1, "ssprk2": 2, "ssprk3": 3}[pb.stepper[0]]
     flops_pt = FLOPS_PER_PT.get((k, rk))
+    nc = pb.n_t // pb.m
 
-    # finite input iterate: the serial solution's C-points
-    serial = P.serial.march(steppers[0], u0, pb.n_t)
-    h = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
-    h._c[h._cur].copy_(serial[::pb.m, 0])
-    h._pristine = False
-    h.f_relax(0)
+    # finite input iterate: the serial solution's C-points (this rank's slab)
+    steppers1 = pb.steppers(tg1)
+    serial = P.serial.march(steppers1[0], u0, pb.n_t)
+    if world == 1:
+        tg, steppers = tg1, steppers1
+        h = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+    else:
+        # weak scaling: the time axis grows with the number of GPUs, each rank
+        # owning the same 1024 CF-intervals; one boundary state is exchanged
+        # per C-relaxation (distributed.py)
+        from paper_2104_09404_b200.distributed import DistMgritHierarchy
+        tg = P.TemporalGrid(tg1.horizon * world, pb.n_t * world)
+        steppers = P.build_steppers(pb.model_obj(), sg, tg, n_levels=pb.n_levels, m=pb.m,
+                                    weno_order=pb.weno_order, stepper=pb.stepper,
+                                    epsilon=pb.epsilon)
+        h = DistMgritHierarchy(steppers, u0, tg, sg, pb.options())
+    h.load_c_points(serial[::pb.m, 0])
     traj = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    # kernel-level events: wrap every launch of a step
-    kern_ms = []
+    def materialise(out):
+        if world == 1:
+            return h.fine_values(out=out)
+        out.view(-1, pb.n_x).copy_(h._local_values())
+        return out
 
     def step(record_kernels=False):
         if record_kernels:
@@ -261,11 +275,11 @@ def run_ours(args):
             e[1].record(stream)
             h.f_relax(0)
             e[2].record(stream)
-            h.fine_values(out=traj)   # F-relax with every F-point stored
+            materialise(traj)     # F-relax with every F-point stored
             e[3].record(stream)
             return e
         h.relax(0)
-        h.fine_values(out=traj)
+        materialise(traj)
         return None
 
     for _ in range(args.warmup):
@@ -304,7 +318,6 @@ def run_ours(args):
     value = units * args.steps * world / (total_ms * 1e-3)
 
     # ---- end to end through the public API with host buffers --------------
-    nc = pb.n_t // pb.m
     host_in = torch.empty(nc + 1, pb.n_x, dtype=torch.float64).pin_memory()
     host_in.copy_(serial[::pb.m, 0].cpu())
     host_out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
@@ -316,18 +329,25 @@ def run_ours(args):
         a.record(stream)
         h.load_c_points(host_in)            # H2D of the step's input iterate
         h.relax(0)
-        host_out.copy_(h.fine_values(out=traj), non_blocking=True)   # D2H
+        host_out.copy_(materialise(traj), non_blocking=True)   # D2H
         b.record(stream)
         if i >= args.warmup:
             e2e_ms.append((a, b))
     torch.cuda.synchronize()
     e2e_total = sum(a.elapsed_time(b) for a, b in e2e_ms)
-    e2e_value = units * args.steps / (e2e_total * 1e-3)
+    te = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = units * args.steps * world / (float(te.item()) * 1e-3)
 
     # ---- one whole MGRIT iteration (V-cycle + residual) from the IC --------
     it_ms = []
     for i in range(4):
-        hi = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+        if world == 1:
+            hi = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+        else:
+            from paper_2104_09404_b200.distributed import DistMgritHierarchy
+            hi = DistMgritHierarchy(steppers, u0, tg, sg, pb.options())
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)

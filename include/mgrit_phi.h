@@ -143,8 +143,10 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream);
 int mgp_sum_partials(const double *partials, int64_t n, int32_t width,
                      double *out, void *stream);
 
-/* Largest nx a single fused field CTA handles (whole field in shared memory). */
-int64_t mgp_max_nx(void);
+/* Largest nx supported for a propagator: 4096 cells per CTA (whole field in
+ * shared memory); WENO5 Burgers fields up to 16 x 4096 cells are split over a
+ * thread-block cluster (nx must then divide into power-of-two slabs). */
+int64_t mgp_max_nx(int32_t weno_k, int32_t model);
 
 /* Library/ABI version and the compile-time WENO tables of degree k, written
  * as cw[4][4], d[4], sm[4][4][4] (row-major, zero padded) so tests can check

@@ -105,6 +105,7 @@ def load():
     lib.mgp_sweep.restype = ctypes.c_int
     lib.mgp_sum_partials.argtypes = [_P, _I64, _I32, _P, _P]
     lib.mgp_sum_partials.restype = ctypes.c_int
+    lib.mgp_max_nx.argtypes = [_I32, _I32]
     lib.mgp_max_nx.restype = _I64
     lib.mgp_abi_version.restype = _I32
     dp = ctypes.POINTER(ctypes.c_double)
@@ -129,5 +130,5 @@ def launch_count() -> int:
     return int(load().mgp_launch_count())
 
 
-def max_nx() -> int:
-    return int(load().mgp_max_nx())
+def max_nx(weno_k: int = 2, model: int = 0) -> int:
+    return int(load().mgp_max_nx(int(weno_k), int(model)))

@@ -14,6 +14,7 @@
 //   flux.py:70-88    global LF speed and flux;  flux.py:159-161 rhs
 //   models.py:107-117 Burgers flux / speed
 //   stepper.py:50-62 SSP-RK1/2/3;  mgrit.py:168-270 level operations.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
@@ -244,30 +245,60 @@ struct Consts {
     int dx_pow2;
 };
 
-// One field in shared memory; thread `run` owns interfaces and cells
-// [run*P, run*P + P) of the periodic mesh.
-template <int K, int REG, int MODEL, int P>
+namespace cg = cooperative_groups;
+
+// Barrier over the CTAs that share one field: the CTA itself (CS = 1) or its
+// thread-block cluster (CS > 1; release/acquire, so shared-memory writes into
+// other CTAs of the cluster are visible after it).
+template <int CS>
+__device__ __forceinline__ void field_sync() {
+    if (CS == 1) {
+        __syncthreads();
+    } else {
+        cg::this_cluster().sync();
+    }
+}
+
+// One field, held in shared memory by one CTA (CS = 1) or split into CS
+// contiguous slabs over a thread-block cluster (CS > 1, for meshes larger
+// than one SM's shared memory and for short sequential marches).  Local cell
+// t of the slab is global cell c0 + t; thread `run` owns local interfaces
+// and cells [run*P, run*P + P).  With CS > 1 the periodic halo comes from
+// the neighbouring CTAs (their boundary cells are stored straight into this
+// CTA's halo through distributed shared memory when committed), the states of
+// the interface just left of the slab are pushed by the left neighbour, and
+// alpha is reduced over the cluster.
+template <int K, int REG, int MODEL, int P, int CS>
 struct Field {
-    static constexpr int H = K + 1;  // periodic halo cells on each side
-    int nx, run, i0;
-    double *s_u;   // stage input, cell c at s_u[sk(c + H)], c in [-H, nx + H)
+    static constexpr int H = K + 1;  // halo cells on each side
+    int ns, run, i0, q;
+    double *s_u;   // stage input, local cell t at s_u[sk(t + H)], t in [-H, ns + H)
     double *s_L;   // left states, then interface fluxes, at s_L[sk(i)]
     double *s_R;   // right states, then results, at s_R[sk(i)]
-    double *s_u0;  // RK base state of the cells, at s_u0[sk(c)]
+    double *s_u0;  // RK base state of the cells, at s_u0[sk(t)]
     unsigned long long *s_red;
+    double *s_edge;                // [2] states of the interface left of the slab
+    unsigned long long *s_cmax;    // [CS] per-CTA alpha bits
+    double *r_u_left, *r_u_right;  // neighbours' s_u (distributed shared memory)
+    double *r_edge_right;          // right neighbour's s_edge
 
-    __device__ __forceinline__ double cell(int c) const { return s_u[sk(c + H)]; }
-    __device__ __forceinline__ void put(int c, double v) {
-        s_u[sk(c + H)] = v;
-        if (c < H) s_u[sk(nx + H + c)] = v;
-        if (c >= nx - H) s_u[sk(c - (nx - H))] = v;
+    __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
+    __device__ __forceinline__ void put(int t, double v) {
+        s_u[sk(t + H)] = v;
+        if (CS == 1) {
+            if (t < H) s_u[sk(ns + H + t)] = v;
+            if (t >= ns - H) s_u[sk(t - (ns - H))] = v;
+        } else {
+            if (t < H) r_u_left[sk(ns + H + t)] = v;
+            if (t >= ns - H) r_u_right[sk(t - ns + H)] = v;
+        }
     }
 
     // Left/right interface states of the owned run -> s_L, s_R; returns the
     // bits of this thread's NaN-propagating max |u| (Burgers).
     __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
         unsigned long long m = 0;
-        const int n = (nx - i0 < P) ? nx - i0 : P;
+        const int n = (ns - i0 < P) ? ns - i0 : P;
         if (n <= 0) return 0;
         constexpr bool kCheck = (MODEL == MGP_MODEL_ADVECTION);
         if (K == 0) {
@@ -285,6 +316,10 @@ struct Field {
                 }
                 s_L[sk(i)] = ul;
                 s_R[sk(i)] = ur;
+                if (CS > 1 && i == ns - 1) {
+                    r_edge_right[0] = ul;
+                    r_edge_right[1] = ur;
+                }
                 if (MODEL == MGP_MODEL_BURGERS) {
                     m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
                     if (!is_finite(c0)) m = kNaNBits;
@@ -341,6 +376,10 @@ struct Field {
             }
             s_L[sk(i)] = ul;
             s_R[sk(i)] = ur;
+            if (CS > 1 && i == ns - 1) {
+                r_edge_right[0] = ul;
+                r_edge_right[1] = ur;
+            }
             if (MODEL == MGP_MODEL_BURGERS) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
                 if (bad_here) m = kNaNBits;
@@ -357,6 +396,19 @@ struct Field {
     // A = SemiDiscreteOperator.rhs(s_u) for the owned cells (flux.py:70-88,
     // 159-161).  Precondition: s_u complete (caller synchronised).  On
     // return A[] holds the owned cells' rhs; s_u is unchanged.
+    __device__ __forceinline__ double lf(const Consts &k, double ul, double ur,
+                                         double half_alpha) const {
+        double fl, fr;
+        if (MODEL == MGP_MODEL_BURGERS) {
+            fl = (0.5 * ul) * ul;
+            fr = (0.5 * ur) * ur;
+        } else {
+            fl = k.speed * ul;
+            fr = k.speed * ur;
+        }
+        return (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
+    }
+
     __device__ __forceinline__ void rhs(const Consts &k, double *A) {
         unsigned long long m = reconstruct(k);
         double half_alpha;
@@ -370,32 +422,36 @@ struct Field {
             m = s_red[0];
             const int nw = (blockDim.x + 31) >> 5;
             for (int w = 1; w < nw; ++w) m = umax64(m, s_red[w]);
+            if (CS > 1) {
+                if (threadIdx.x == 0) {
+                    cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+                    for (int j = 0; j < CS; ++j) cl.map_shared_rank(s_cmax, j)[q] = m;
+                }
+                field_sync<CS>();   // also publishes the pushed edge states
+                m = s_cmax[0];
+#pragma unroll
+                for (int j = 1; j < CS; ++j) m = umax64(m, s_cmax[j]);
+            }
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         } else {
             half_alpha = k.half_alpha_adv;
+            if (CS > 1) field_sync<CS>();
         }
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int i = i0 + p;
-            if (i < nx) {
-                const double ul = s_L[sk(i)], ur = s_R[sk(i)];
-                double fl, fr;
-                if (MODEL == MGP_MODEL_BURGERS) {
-                    fl = (0.5 * ul) * ul;
-                    fr = (0.5 * ur) * ur;
-                } else {
-                    fl = k.speed * ul;
-                    fr = k.speed * ur;
-                }
-                s_L[sk(i)] = (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
-            }
+            if (i < ns) s_L[sk(i)] = lf(k, s_L[sk(i)], s_R[sk(i)], half_alpha);
         }
         __syncthreads();
 #pragma unroll
         for (int p = 0; p < P; ++p) {
             const int c = i0 + p;
-            if (c < nx) {
-                const double fm = s_L[sk(c == 0 ? nx - 1 : c - 1)];
+            if (c < ns) {
+                double fm;
+                if (c > 0) fm = s_L[sk(c - 1)];
+                else if (CS == 1) fm = s_L[sk(ns - 1)];
+                else fm = lf(k, s_edge[0], s_edge[1], half_alpha);
                 const double neg = -(s_L[sk(c)] - fm);
                 A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
             }
@@ -412,12 +468,12 @@ struct Field {
     __device__ __forceinline__ void phi(const Consts &k, int rk) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-            if (i0 + p < nx) s_u0[sk(i0 + p)] = cell(i0 + p);
+            if (i0 + p < ns) s_u0[sk(i0 + p)] = cell(i0 + p);
         const int stages = rk == 0 ? 1 : rk;
         // one call site of the reconstruction for every stage (code size)
 #pragma unroll 1
         for (int sg = 0; sg < stages; ++sg) {
-            if (sg > 0) __syncthreads();  // committed stage values visible
+            if (sg > 0) field_sync<CS>();  // committed stage values (and halos) visible
             double A[P];
             rhs(k, A);
             double st[P];
@@ -442,18 +498,18 @@ struct Field {
     }
 
     __device__ __forceinline__ double stage(int p) const {
-        return (i0 + p < nx) ? cell(i0 + p) : 0.0;
+        return (i0 + p < ns) ? cell(i0 + p) : 0.0;
     }
 
     __device__ __forceinline__ void commit(const double *v) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-            if (i0 + p < nx) put(i0 + p, v[p]);
+            if (i0 + p < ns) put(i0 + p, v[p]);
     }
     __device__ __forceinline__ void store_res(const double *v) {
 #pragma unroll
         for (int p = 0; p < P; ++p)
-            if (i0 + p < nx) s_R[sk(i0 + p)] = v[p];
+            if (i0 + p < ns) s_R[sk(i0 + p)] = v[p];
     }
 };
 
@@ -467,49 +523,69 @@ __device__ __forceinline__ double g_value(int mode, const double *g, int c) {
     return mode == MGP_G_ARRAY ? g[c] : 0.0;
 }
 
-template <int K, int REG, int MODEL, int P, int REGS>
+template <int K, int REG, int MODEL, int P, int REGS, int CS>
 __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
     extern __shared__ double smem[];
-    using F = Field<K, REG, MODEL, P>;
+    using F = Field<K, REG, MODEL, P, CS>;
     F f;
     const int nx = (int)a.phi.nx;
+    const int ns = nx / CS;            // cells of this CTA's slab
+    const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
+    const int c0 = q * ns;             // global index of local cell 0
     const int tid = threadIdx.x, nt = blockDim.x;
-    f.nx = nx;
+    f.ns = ns;
+    f.q = q;
     f.run = tid;
     f.i0 = tid * P;
     f.s_u = smem;
-    f.s_L = f.s_u + sk_size(nx + 2 * F::H);
-    f.s_R = f.s_L + sk_size(nx);
-    f.s_u0 = f.s_R + sk_size(nx);
-    double *s_sum = f.s_u0 + sk_size(nx);
-    f.s_red = reinterpret_cast<unsigned long long *>(s_sum + 3 * 32);
+    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
+    f.s_R = f.s_L + sk_size(ns);
+    f.s_u0 = f.s_R + sk_size(ns);
+    double *s_sum = f.s_u0 + sk_size(ns);      // [3 * 32]
+    double *s_psum = s_sum + 3 * 32;           // [3 * CS] cluster partials
+    f.s_edge = s_psum + 3 * CS;                // [2]
+    f.s_cmax = reinterpret_cast<unsigned long long *>(f.s_edge + 2);   // [CS]
+    f.s_red = f.s_cmax + CS;                   // [32]
+    if (CS > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        f.r_u_left = cl.map_shared_rank(f.s_u, (q + CS - 1) % CS);
+        f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
+        f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
+    }
     const int rk = a.phi.rk_order;
     const int total = a.n_steps + (a.tail != MGP_TAIL_NONE ? 1 : 0);
+    const int64_t first = blockIdx.x / CS, stride = gridDim.x / CS;
 
-    for (int64_t b = blockIdx.x; b < a.n_chunks; b += gridDim.x) {
+    for (int64_t b = first; b < a.n_chunks; b += stride) {
         double acc_r = 0.0, acc_e = 0.0, acc_n = 0.0;
         const double *x0 = a.start + b * a.start_stride;
         const double *ref = a.ref ? a.ref + b * a.ref_cs : nullptr;
-        for (int c = tid; c < nx; c += nt) {
+        // slab and halo straight from global memory (periodic)
+        for (int t = tid - F::H; t < ns + F::H; t += nt) {
+            int c = c0 + t;
+            c = c < 0 ? c + nx : (c >= nx ? c - nx : c);
             const double v = x0[c];
-            f.put(c, v);
-            if (ref) {
-                const double d = v - ref[c];
-                acc_e = acc_e + d * d;
+            f.s_u[sk(t + F::H)] = v;
+            if (t >= 0 && t < ns) {
+                if (ref) {
+                    const double d = v - ref[c];
+                    acc_e = acc_e + d * d;
+                }
+                if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
             }
-            if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
         }
         for (int s = 1; s <= total; ++s) {
-            __syncthreads();  // s_u complete
+            field_sync<CS>();  // s_u and halos complete
             f.phi(k, rk);
-            __syncthreads();  // results in s_R complete
+            __syncthreads();   // results in s_R complete
             if (s <= a.n_steps) {
                 const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
                 double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
                 const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
-                for (int c = tid; c < nx; c += nt) {
-                    const double v = add_g(f.s_R[sk(c)], a.g_mode, g, c);
-                    f.put(c, v);
+                for (int t = tid; t < ns; t += nt) {
+                    const int c = c0 + t;
+                    const double v = add_g(f.s_R[sk(t)], a.g_mode, g, c);
+                    f.put(t, v);
                     if (st) st[c] = v;
                     if (rs) {
                         const double d = v - rs[c];
@@ -522,8 +598,8 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
             const double *tg = a.tail_g ? a.tail_g + b * a.tg_s : nullptr;
             if (a.tail == MGP_TAIL_PHI) {
                 double *out = a.tail_out + b * a.to_s;
-                for (int c = tid; c < nx; c += nt)
-                    out[c] = add_g(f.s_R[sk(c)], a.tail_g_mode, tg, c);
+                for (int t = tid; t < ns; t += nt)
+                    out[c0 + t] = add_g(f.s_R[sk(t)], a.tail_g_mode, tg, c0 + t);
             } else if (a.tail == MGP_TAIL_RESTRICT) {
                 // mgrit.py:211-215: g_c = (g_f + phi) - psi;
                 // u_c = phi + g_f (last-step) or u_f (injection)
@@ -531,11 +607,12 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 const double *uf = a.aux2 ? a.aux2 + b * a.aux2_s : nullptr;
                 double *gc = a.tail_out + b * a.to_s;
                 double *uc = a.tail_out2 + b * a.to2_s;
-                for (int c = tid; c < nx; c += nt) {
+                for (int t = tid; t < ns; t += nt) {
+                    const int c = c0 + t;
                     const double p = phi[c];
                     const double left =
                         (a.tail_g_mode == MGP_G_NONE) ? p : g_value(a.tail_g_mode, tg, c) + p;
-                    gc[c] = left - f.s_R[sk(c)];
+                    gc[c] = left - f.s_R[sk(t)];
                     uc[c] = (a.guess == MGP_GUESS_LAST_STEP) ? add_g(p, a.tail_g_mode, tg, c)
                                                              : uf[c];
                 }
@@ -543,8 +620,9 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 const double *tgt = a.aux + b * a.aux_s;
                 const bool last = (b == a.n_chunks - 1) && a.ref_last_next;
                 const double *rn = (last && a.ref) ? a.ref + (b + 1) * a.ref_cs : nullptr;
-                for (int c = tid; c < nx; c += nt) {
-                    const double y = f.s_R[sk(c)];
+                for (int t = tid; t < ns; t += nt) {
+                    const int c = c0 + t;
+                    const double y = f.s_R[sk(t)];
                     const double pred =
                         (a.tail_g_mode == MGP_G_NONE) ? y : g_value(a.tail_g_mode, tg, c) + y;
                     const double u = tgt[c];
@@ -561,7 +639,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
             }
         }
         if (a.partials) {
-            // fixed-order block reduction (deterministic for a given nt)
+            // fixed-order reduction: warps, CTA, then cluster ranks in order
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 acc_r += __shfl_xor_sync(0xffffffffu, acc_r, o);
@@ -579,10 +657,23 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 double t = 0.0;
                 const int nw = (nt + 31) >> 5;
                 for (int w = 0; w < nw; ++w) t = t + s_sum[3 * w + tid];
-                a.partials[3 * b + tid] = t;
+                if (CS == 1) {
+                    a.partials[3 * b + tid] = t;
+                } else {
+                    cg::cluster_group cl = cg::this_cluster();
+                    cl.map_shared_rank(s_psum, 0)[3 * q + tid] = t;
+                }
+            }
+            if (CS > 1) {
+                field_sync<CS>();
+                if (q == 0 && tid < 3) {
+                    double t = 0.0;
+                    for (int j = 0; j < CS; ++j) t = t + s_psum[3 * j + tid];
+                    a.partials[3 * b + tid] = t;
+                }
             }
         }
-        __syncthreads();  // shared buffers are reused by the next chunk
+        field_sync<CS>();  // shared buffers are reused by the next chunk
     }
 }
 
@@ -653,34 +744,55 @@ int run_length(int64_t nx, int64_t n_chunks) {
     return p;
 }
 
-int threads_for(int64_t nx, int p) {
-    int64_t nt = (nx + p - 1) / p;
+int threads_for(int64_t ns, int p) {
+    int64_t nt = (ns + p - 1) / p;
     nt = (nt + 31) / 32 * 32;
     return (int)nt;
 }
 
-size_t smem_bytes(int64_t nx, int k) {
+size_t smem_bytes(int64_t ns, int k, int cs) {
     const int H = k + 1;
-    return sizeof(double) * (size_t)(sk_size((int)nx + 2 * H) + 3 * sk_size((int)nx) + 3 * 32) +
-           sizeof(unsigned long long) * 32;
+    return sizeof(double) * (size_t)(sk_size((int)ns + 2 * H) + 3 * sk_size((int)ns) + 3 * 32 +
+                                     3 * cs + 2) +
+           sizeof(unsigned long long) * (size_t)(cs + 32);
 }
 
-template <int K, int REG, int MODEL, int P, int REGS>
+template <int K, int REG, int MODEL, int P, int REGS, int CS>
 int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
-    const int nt = threads_for(a.phi.nx, P);
-    const size_t sm = smem_bytes(a.phi.nx, K);
-    auto kern = sweep_kernel<K, REG, MODEL, P, REGS>;
+    const int64_t ns = a.phi.nx / CS;
+    const int nt = threads_for(ns, P);
+    const size_t sm = smem_bytes(ns, K, CS);
+    auto kern = sweep_kernel<K, REG, MODEL, P, REGS, CS>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024) != cudaSuccess)
             return MGP_ECUDA;
+        if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                           1) != cudaSuccess)
+            return MGP_ECUDA;
         attr_set = true;
     }
     int64_t grid = a.n_chunks;
-    if (grid > (int64_t)1 << 30) grid = (int64_t)1 << 30;
+    if (grid > ((int64_t)1 << 30) / CS) grid = ((int64_t)1 << 30) / CS;
     const Consts k = make_consts(a.phi);
-    kern<<<(unsigned)grid, nt, sm, st>>>(a, k);
+    if (CS == 1) {
+        kern<<<(unsigned)grid, nt, sm, st>>>(a, k);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(grid * CS));
+        cfg.blockDim = dim3(nt);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k) != cudaSuccess) return MGP_ECUDA;
+    }
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
@@ -689,30 +801,71 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
 #define MGP_REGS 128
 #endif
 
+int env_int(const char *name) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : 0;
+}
+
+// Cluster size for a field: meshes above one SM's capacity must be split
+// (WENO5 Burgers only, up to 16 x 4096 cells); single-field marches of the
+// sequential coarse solve are split for latency (MGP_MARCH_CS overrides).
+int cluster_size(const mgp_sweep_args &a) {
+    const int64_t nx = a.phi.nx;
+    const bool cl_ok = a.phi.weno_k == 2 && a.phi.model == MGP_MODEL_BURGERS;
+    if (nx > kMaxNx) {
+        int cs = 2;
+        while (nx / cs > kMaxNx || nx % cs) cs *= 2;
+        return cs;
+    }
+    if (cl_ok && a.n_chunks == 1) {
+        static int env = -1;
+        if (env < 0) env = env_int("MGP_MARCH_CS");
+        int cs = env > 0 ? env : 4;
+        while (cs > 1 && (nx % cs || nx / cs < 64)) cs /= 2;
+        return cs;
+    }
+    return 1;
+}
+
 template <int K, int REG, int MODEL, int P>
 int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
 #ifdef MGP_EXPERIMENT
     // register-budget experiments (tools/): MGP_MAXREG selects the variant
     static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("MGP_MAXREG");
-        env = e ? atoi(e) : 0;
-    }
+    if (env < 0) env = env_int("MGP_MAXREG");
     if (K == 2 && MODEL == MGP_MODEL_BURGERS && P >= 4) {
         switch (env) {
-            case 80: return launch_t<K, REG, MODEL, P, 80>(a, st);
-            case 96: return launch_t<K, REG, MODEL, P, 96>(a, st);
-            case 104: return launch_t<K, REG, MODEL, P, 104>(a, st);
-            case 112: return launch_t<K, REG, MODEL, P, 112>(a, st);
+            case 96: return launch_t<K, REG, MODEL, P, 96, 1>(a, st);
+            case 112: return launch_t<K, REG, MODEL, P, 112, 1>(a, st);
             default: break;
         }
     }
 #endif
-    return launch_t<K, REG, MODEL, P, MGP_REGS>(a, st);
+    return launch_t<K, REG, MODEL, P, MGP_REGS, 1>(a, st);
 }
 
 template <int K, int REG, int MODEL>
 int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
+    const int cs = cluster_size(a);
+    if (cs > 1) {
+      if constexpr (K != 2 || MODEL != MGP_MODEL_BURGERS) {
+        return MGP_EINVAL;
+      } else {
+        // slabs: P = 8 above 512 cells per CTA, P = 1 (latency) otherwise
+        const bool wide = a.phi.nx / cs > 512;
+        switch (cs) {
+            case 2: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 2>(a, st)
+                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 2>(a, st);
+            case 4: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 4>(a, st)
+                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 4>(a, st);
+            case 8: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 8>(a, st)
+                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 8>(a, st);
+            case 16: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 16>(a, st)
+                                 : launch_t<K, REG, MODEL, 1, MGP_REGS, 16>(a, st);
+        }
+        return MGP_EINVAL;
+      }
+    }
     switch (run_length(a.phi.nx, a.n_chunks)) {
         case 1: return launch_r<K, REG, MODEL, 1>(a, st);
         case 2: return launch_r<K, REG, MODEL, 2>(a, st);
@@ -738,6 +891,10 @@ int launch_m(const mgp_sweep_args &a, cudaStream_t st) {
     return MGP_EINVAL;
 }
 
+int64_t max_nx_for(int k, int model) {
+    return (k == 2 && model == MGP_MODEL_BURGERS) ? 16 * kMaxNx : kMaxNx;
+}
+
 int validate(const mgp_sweep_args *a) {
     if (!a) return MGP_EINVAL;
     const mgp_phi &p = a->phi;
@@ -745,7 +902,14 @@ int validate(const mgp_sweep_args *a) {
     if (p.weno_k < 0 || p.weno_k > 3) return MGP_EINVAL;
     if (p.rk_order < 0 || p.rk_order > 3) return MGP_EINVAL;
     if (p.regime != MGP_SUM_SEQ && p.regime != MGP_SUM_LANE2) return MGP_EINVAL;
-    if (p.nx < 2 * p.weno_k + 1 || p.nx > kMaxNx) return MGP_EINVAL;
+    if (p.nx < 2 * p.weno_k + 1 || p.nx > max_nx_for(p.weno_k, p.model)) return MGP_EINVAL;
+    if (p.nx > kMaxNx && p.nx % (((p.nx + kMaxNx - 1) / kMaxNx + 0)) != 0) {
+        int cs = 2;
+        while (p.nx / cs > kMaxNx || p.nx % cs) {
+            cs *= 2;
+            if (cs > 16) return MGP_EINVAL;
+        }
+    }
     if (!(p.dx > 0.0) || !(p.epsilon > 0.0)) return MGP_EINVAL;
     if (a->n_chunks < 0 || a->n_steps < 0 || !a->start) return MGP_EINVAL;
     if (a->g_mode < MGP_G_NONE || a->g_mode > MGP_G_ARRAY) return MGP_EINVAL;
@@ -790,7 +954,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
-int64_t mgp_max_nx(void) { return kMaxNx; }
+int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
 int32_t mgp_abi_version(void) { return 1; }
 

@@ -166,9 +166,13 @@ class MgritHierarchy:
             raise DimensionError(f"initial state must be (1, N), got {tuple(u0.shape)}")
         self.nx = nx = u0.shape[1]
         self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
-        if not dev.emulated() and nx > dev._lib.max_nx():
-            raise ConfigError(f"N_x = {nx} exceeds the single-CTA field limit "
-                              f"{dev._lib.max_nx()} of this build")
+        if not dev.emulated():
+            for s in self.steppers:
+                op = s.operator
+                lim = dev._lib.max_nx(op.config.weno.degree, op.model.abi_model)
+                if nx > lim:
+                    raise ConfigError(f"N_x = {nx} exceeds the field limit {lim} of this "
+                                      f"build for WENO{op.config.weno.order}")
         self._u0 = u0[0].contiguous()
         self.n = [time_grid.n_steps // m ** l for l in range(L)]
         self.levels = [MgritLevel(self, l, time_grid.dt * m ** l, self.n[l], steppers[l])

@@ -55,7 +55,7 @@ def test_device_tables_equal_rational_tables(k):
 def test_abi_constants():
     lib = _lib.load()
     assert lib.mgp_abi_version() == 1
-    assert lib.mgp_max_nx() >= 4096
+    assert lib.mgp_max_nx(2, 0) == 65536 and lib.mgp_max_nx(1, 0) == 4096
     assert lib.mgp_launch_count() >= 0
     hdr = open(_lib.HEADER_PATH).read()
     for name, val in [("MGP_SUM_SEQ", _lib.SUM_SEQ), ("MGP_SUM_LANE2", _lib.SUM_LANE2),

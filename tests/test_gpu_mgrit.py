@@ -167,3 +167,26 @@ def test_c3_full_size_row0_and_divergence():
                            return_trajectory=False)
     assert abs(rec.residuals[0] - 6.582632) < 5e-6
     assert rec.diverged_at == 1
+
+
+def test_large_mesh_mgrit_on_clusters():
+    """nx = 8192 (two-CTA clusters for every level operation, cluster-reduced
+    residual partials) against the oracle restatement."""
+    pb = P.Problem(name="big", n_x=8192, n_t=32, cfl=0.05, n_modes=6, n_levels=3, m=4,
+                   relaxation="fcf", max_iters=2)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    ref = P.serial.march(steppers[0], u0, pb.n_t)
+    traj, rec = P.mgrit_solve(steppers, u0, tg, pb.space_grid(), pb.options(), reference=ref)
+    ost = [oracle.OracleStepper(k=2, rk_order=3, dt=tg.dt * 4 ** l, dx=1.0 / 8192)
+           for l in range(3)]
+    oref = mgrit_oracle.march(ost[0], u0, pb.n_t)
+    assert np.array_equal(ref.cpu().numpy(), oref)
+    otraj, orec = mgrit_oracle.mgrit_solve(ost, u0, pb.n_t, tg.dt,
+                                           mgrit_oracle.Options(n_levels=3, m=4,
+                                                                relaxation="fcf", max_iters=2),
+                                           reference=oref)
+    assert np.array_equal(traj.values, otraj)
+    np.testing.assert_allclose(rec.residuals, orec.residuals, rtol=1e-10)
+    np.testing.assert_allclose(rec.errors, orec.errors, rtol=1e-10)
