@@ -91,6 +91,25 @@ constexpr int64_t kMaxNx = (int64_t)kMaxThreads * kMaxRun;
 
 unsigned long long g_launches = 0;
 
+#ifdef MGP_TRACE
+__device__ long long g_trace[8192];
+__device__ int g_trace_n;
+__device__ __forceinline__ void trace(int tag) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const int i = g_trace_n;
+        if (i < 4096) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            g_trace[2 * i] = tag;
+            g_trace[2 * i + 1] = t;
+            g_trace_n = i + 1;
+        }
+    }
+}
+#else
+__device__ __forceinline__ void trace(int) {}
+#endif
+
 __device__ __forceinline__ bool is_finite(double x) {
     return (__double2hiint(x) & 0x7FF00000) != 0x7FF00000;
 }
@@ -105,6 +124,16 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
 }
 
 constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
+
+#ifndef MGP_SLIDE_UNROLL
+#define MGP_SLIDE_UNROLL 1
+#endif
+#ifndef MGP_SKEW
+#define MGP_SKEW 0
+#endif
+#define MGP_PRAGMA(x) _Pragma(#x)
+#define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
+#define MGP_UNROLL(n) MGP_UNROLL_(n)
 
 // Shared-memory index of element t: one pad word per 16 elements, so that
 // the lanes of a warp walking runs of P in {1,2,4,8} consecutive cells hit
@@ -175,7 +204,7 @@ __device__ __forceinline__ double cand_right(const double *win, int r) {
 // Products of left beta_s(m): cells m-s+a -> win[K-s+a].  Returns the
 // forward (a-major) sum; when RIGHT, also the reverse-order sum, which is
 // right beta_{K-s}(m-1).
-template <int K, bool RIGHT>
+template <int K, bool RIGHT, bool LEFT = true>
 __device__ __forceinline__ void beta_block(const double *win, int s, double &fwd,
                                            double &rev) {
     constexpr int N = (K + 1) * (K + 1);
@@ -185,10 +214,12 @@ __device__ __forceinline__ void beta_block(const double *win, int s, double &fwd
 #pragma unroll
         for (int b = 0; b <= K; ++b)
             p[a * (K + 1) + b] = (win[K - s + a] * c_sm[K][s][a][b]) * win[K - s + b];
-    double f = p[0];
+    if (LEFT) {
+        double f = p[0];
 #pragma unroll
-    for (int t = 1; t < N; ++t) f = f + p[t];
-    fwd = f;
+        for (int t = 1; t < N; ++t) f = f + p[t];
+        fwd = f;
+    }
     if (RIGHT) {
         double g = p[N - 1];
 #pragma unroll
@@ -220,7 +251,8 @@ __device__ __forceinline__ double weno_value_ieee(const double *beta, const doub
 }
 
 template <int K>
-__device__ __forceinline__ double weno_value(const double *beta, const double *q, double eps) {
+__device__ __forceinline__ double weno_value(const double *beta, const double *q, double eps,
+                                             bool moot = false) {
     bool bad = false;
     double raw[K + 1];
 #pragma unroll
@@ -235,7 +267,10 @@ __device__ __forceinline__ double weno_value(const double *beta, const double *q
     double v = mgp::div_fast(raw[0], R, bad) * q[0];
 #pragma unroll
     for (int r = 1; r <= K; ++r) v = v + mgp::div_fast(raw[r], R, bad) * q[r];
-    if (bad) v = weno_value_ieee<K>(beta, q, eps);
+    // `moot`: the value cannot reach the result (Burgers with a non-finite
+    // cell in the field: alpha is NaN and every flux NaN), so skip the
+    // slow exact recomputation on such data
+    if (bad && !moot) v = weno_value_ieee<K>(beta, q, eps);
     return v;
 }
 
@@ -271,6 +306,10 @@ __device__ __forceinline__ void field_sync() {
 template <int K, int REG, int MODEL, int P, int CS>
 struct Field {
     static constexpr int H = K + 1;  // halo cells on each side
+    // P = 0: latency mode for sequential marches -- two threads per interface
+    // (warps alternate between left and right states), one cell per thread
+    // in the cell phases.  Otherwise P cells/interfaces per thread.
+    static constexpr int PC = P == 0 ? 1 : P;
     int ns, run, i0, q;
     double *s_u;   // stage input, local cell t at s_u[sk(t + H)], t in [-H, ns + H)
     double *s_L;   // left states, then interface fluxes, at s_L[sk(i)]
@@ -281,6 +320,10 @@ struct Field {
     unsigned long long *s_cmax;    // [CS] per-CTA alpha bits
     double *r_u_left, *r_u_right;  // neighbours' s_u (distributed shared memory)
     double *r_edge_right;          // right neighbour's s_edge
+    // barrier over the CTAs sharing the field (hardware cluster barrier; an
+    // mbarrier-based all-to-all with one arriving thread per CTA measured
+    // 1.8-2.5x slower per stage on B200)
+    __device__ __forceinline__ void sync() { field_sync<CS>(); }
 
     __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
     __device__ __forceinline__ void put(int t, double v) {
@@ -298,9 +341,51 @@ struct Field {
     // bits of this thread's NaN-propagating max |u| (Burgers).
     __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
         unsigned long long m = 0;
-        const int n = (ns - i0 < P) ? ns - i0 : P;
-        if (n <= 0) return 0;
         constexpr bool kCheck = (MODEL == MGP_MODEL_ADVECTION);
+        if (P == 0 && K > 0) {
+            const int tid = threadIdx.x;
+            const int side = (tid >> 5) & 1;              // warp-uniform
+            const int i = ((tid >> 6) << 5) + (tid & 31);
+            if (i >= ns) return 0;
+            const int ctr = i + side;                      // window centre
+            double win[2 * K + 1];
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) win[t] = cell(ctr - K + t);
+            bool badw = false;
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) badw |= !is_finite(win[t]);
+            double b[K + 1], q[K + 1];
+            if (side == 0) {
+#pragma unroll
+                for (int s2 = 0; s2 <= K; ++s2) {
+                    double dummy;
+                    beta_block<K, false, true>(win, s2, b[s2], dummy);
+                }
+#pragma unroll
+                for (int r = 0; r <= K; ++r) q[r] = cand_left<K, REG>(win, r);
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 <= K; ++s2) {
+                    double dummy;
+                    beta_block<K, true, false>(win, s2, dummy, b[K - s2]);
+                }
+#pragma unroll
+                for (int r = 0; r <= K; ++r) q[r] = cand_right<K, REG>(win, r);
+            }
+            const bool moot = MODEL == MGP_MODEL_BURGERS && badw;
+            double v = weno_value<K>(b, q, k.eps, moot);
+            if (kCheck && badw) v = __longlong_as_double(kNaNBits);
+            if (side == 0) s_L[sk(i)] = v;
+            else s_R[sk(i)] = v;
+            if (CS > 1 && i == ns - 1) r_edge_right[side] = v;
+            if (MODEL == MGP_MODEL_BURGERS) {
+                m = abs_bits(v);
+                if (side == 0 && !is_finite(win[K])) m = kNaNBits;
+            }
+            return m;
+        }
+        const int n = (ns - i0 < PC) ? ns - i0 : PC;
+        if (n <= 0) return 0;
         if (K == 0) {
             // beta = 0, omega = raw/raw (1, or NaN when 1/eps^2 overflows)
             double c0 = cell(i0);
@@ -340,7 +425,72 @@ struct Field {
         }
 #pragma unroll
         for (int r = 0; r <= K; ++r) ql[r] = cand_left<K, REG>(win, r);
-#pragma unroll 1
+#if MGP_SKEW
+        // Skewed pipeline: iteration p forms the products of the left state
+        // at i+1 while finishing the weights of left(i) and right(i-1), whose
+        // inputs are already complete -- two independent division chains
+        // overlap the product/sum work of the next interface.
+        double br_prev[K + 1], qr_prev[K + 1];
+        bool badr_prev = false, moot_prev = false;
+        MGP_UNROLL(MGP_SLIDE_UNROLL)
+        for (int p = 0; p <= n; ++p) {
+            const int i = i0 + p;
+            const bool body = p < n;
+            bool bad_left = false, bad_right = false, moot = false;
+            double bl_next[K + 1], br[K + 1], ql_next[K + 1], qr[K + 1];
+            if (body) {
+                const bool bad_here = !is_finite(win[K]);
+                if (kCheck) {
+#pragma unroll
+                    for (int t = 0; t <= 2 * K; ++t) bad_left |= !is_finite(win[t]);
+                }
+#pragma unroll
+                for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
+                win[2 * K] = cell(i + 1 + K);
+                if (kCheck) {
+#pragma unroll
+                    for (int t = 0; t <= 2 * K; ++t) bad_right |= !is_finite(win[t]);
+                }
+#pragma unroll
+                for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl_next[s], br[K - s]);
+#pragma unroll
+                for (int r = 0; r <= K; ++r) {
+                    ql_next[r] = cand_left<K, REG>(win, r);
+                    qr[r] = cand_right<K, REG>(win, r);
+                }
+                if (MODEL == MGP_MODEL_BURGERS) {
+#pragma unroll
+                    for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(win[t]);
+                    moot |= bad_here;
+                    if (bad_here) m = kNaNBits;
+                }
+                double ul = weno_value<K>(bl, ql, k.eps, moot);
+                if (kCheck && bad_left) ul = __longlong_as_double(kNaNBits);
+                s_L[sk(i)] = ul;
+                if (MODEL == MGP_MODEL_BURGERS) m = umax64(m, abs_bits(ul));
+                if (CS > 1 && i == ns - 1) r_edge_right[0] = ul;
+            }
+            if (p > 0) {
+                double ur = weno_value<K>(br_prev, qr_prev, k.eps, moot_prev);
+                if (kCheck && badr_prev) ur = __longlong_as_double(kNaNBits);
+                s_R[sk(i - 1)] = ur;
+                if (MODEL == MGP_MODEL_BURGERS) m = umax64(m, abs_bits(ur));
+                if (CS > 1 && i - 1 == ns - 1) r_edge_right[1] = ur;
+            }
+            if (body) {
+#pragma unroll
+                for (int s = 0; s <= K; ++s) {
+                    bl[s] = bl_next[s];
+                    ql[s] = ql_next[s];
+                    br_prev[s] = br[s];
+                    qr_prev[s] = qr[s];
+                }
+                badr_prev = bad_right;
+                moot_prev = moot;
+            }
+        }
+#else
+        MGP_UNROLL(MGP_SLIDE_UNROLL)
         for (int p = 0; p < n; ++p) {
             const int i = i0 + p;
             // window of the left state at i+1; the nonfinite flag covers the
@@ -368,8 +518,14 @@ struct Field {
                 ql_next[r] = cand_left<K, REG>(win, r);
                 qr[r] = cand_right<K, REG>(win, r);
             }
-            double ul = weno_value<K>(bl, ql, k.eps);
-            double ur = weno_value<K>(br, qr, k.eps);
+            bool moot = false;
+            if (MODEL == MGP_MODEL_BURGERS) {
+#pragma unroll
+                for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(win[t]);
+                moot |= bad_here;
+            }
+            double ul = weno_value<K>(bl, ql, k.eps, moot);
+            double ur = weno_value<K>(br, qr, k.eps, moot);
             if (kCheck) {
                 if (bad_left) ul = __longlong_as_double(kNaNBits);
                 if (bad_right) ur = __longlong_as_double(kNaNBits);
@@ -390,6 +546,7 @@ struct Field {
                 ql[s] = ql_next[s];
             }
         }
+#endif
         return m;
     }
 
@@ -410,7 +567,9 @@ struct Field {
     }
 
     __device__ __forceinline__ void rhs(const Consts &k, double *A) {
+        trace(1);
         unsigned long long m = reconstruct(k);
+        trace(2);
         double half_alpha;
         if (MODEL == MGP_MODEL_BURGERS) {
 #pragma unroll
@@ -428,7 +587,7 @@ struct Field {
 #pragma unroll
                     for (int j = 0; j < CS; ++j) cl.map_shared_rank(s_cmax, j)[q] = m;
                 }
-                field_sync<CS>();   // also publishes the pushed edge states
+                sync();   // also publishes the pushed edge states
                 m = s_cmax[0];
 #pragma unroll
                 for (int j = 1; j < CS; ++j) m = umax64(m, s_cmax[j]);
@@ -436,16 +595,17 @@ struct Field {
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         } else {
             half_alpha = k.half_alpha_adv;
-            if (CS > 1) field_sync<CS>();
+            if (CS > 1) sync();
         }
+        trace(3);
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
+        for (int p = 0; p < PC; ++p) {
             const int i = i0 + p;
             if (i < ns) s_L[sk(i)] = lf(k, s_L[sk(i)], s_R[sk(i)], half_alpha);
         }
         __syncthreads();
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
+        for (int p = 0; p < PC; ++p) {
             const int c = i0 + p;
             if (c < ns) {
                 double fm;
@@ -456,6 +616,7 @@ struct Field {
                 A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
             }
         }
+        trace(4);
     }
 
     // res = RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned
@@ -463,23 +624,28 @@ struct Field {
     // s_u complete and synchronised.  Leaves s_u holding the last stage input.
     // The RK base and the stage values live in shared memory (s_u0, s_u), so
     // no per-cell state is held in registers across the reconstruction.
-    __device__ __forceinline__ double u0(int p) const { return s_u0[sk(i0 + p)]; }
+    __device__ __forceinline__ double u0(int p) const {
+        return (i0 + p < ns) ? s_u0[sk(i0 + p)] : 0.0;
+    }
 
     __device__ __forceinline__ void phi(const Consts &k, int rk) {
 #pragma unroll
-        for (int p = 0; p < P; ++p)
+        for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) s_u0[sk(i0 + p)] = cell(i0 + p);
         const int stages = rk == 0 ? 1 : rk;
         // one call site of the reconstruction for every stage (code size)
 #pragma unroll 1
         for (int sg = 0; sg < stages; ++sg) {
-            if (sg > 0) field_sync<CS>();  // committed stage values (and halos) visible
-            double A[P];
+            if (sg > 0) {
+                trace(5);
+                sync();  // committed stage values (and halos) visible
+            }
+            double A[PC];
             rhs(k, A);
-            double st[P];
+            double st[PC];
             const bool last = (sg == stages - 1);
 #pragma unroll
-            for (int p = 0; p < P; ++p) {
+            for (int p = 0; p < PC; ++p) {
                 if (rk == 0) {
                     st[p] = A[p];
                 } else if (sg == 0) {
@@ -503,12 +669,12 @@ struct Field {
 
     __device__ __forceinline__ void commit(const double *v) {
 #pragma unroll
-        for (int p = 0; p < P; ++p)
+        for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) put(i0 + p, v[p]);
     }
     __device__ __forceinline__ void store_res(const double *v) {
 #pragma unroll
-        for (int p = 0; p < P; ++p)
+        for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) s_R[sk(i0 + p)] = v[p];
     }
 };
@@ -536,7 +702,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     f.ns = ns;
     f.q = q;
     f.run = tid;
-    f.i0 = tid * P;
+    f.i0 = tid * F::PC;
     f.s_u = smem;
     f.s_L = f.s_u + sk_size(ns + 2 * F::H);
     f.s_R = f.s_L + sk_size(ns);
@@ -575,7 +741,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
             }
         }
         for (int s = 1; s <= total; ++s) {
-            field_sync<CS>();  // s_u and halos complete
+            f.sync();  // s_u and halos complete
             f.phi(k, rk);
             __syncthreads();   // results in s_R complete
             if (s <= a.n_steps) {
@@ -665,7 +831,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 }
             }
             if (CS > 1) {
-                field_sync<CS>();
+                f.sync();
                 if (q == 0 && tid < 3) {
                     double t = 0.0;
                     for (int j = 0; j < CS; ++j) t = t + s_psum[3 * j + tid];
@@ -673,7 +839,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 }
             }
         }
-        field_sync<CS>();  // shared buffers are reused by the next chunk
+        f.sync();  // shared buffers are reused by the next chunk
     }
 }
 
@@ -745,7 +911,7 @@ int run_length(int64_t nx, int64_t n_chunks) {
 }
 
 int threads_for(int64_t ns, int p) {
-    int64_t nt = (ns + p - 1) / p;
+    int64_t nt = p == 0 ? 2 * ((ns + 31) / 32 * 32) : (ns + p - 1) / p;
     nt = (nt + 31) / 32 * 32;
     return (int)nt;
 }
@@ -820,11 +986,12 @@ int cluster_size(const mgp_sweep_args &a) {
     if (cl_ok && a.n_chunks == 1) {
         static int env = -1;
         if (env < 0) env = env_int("MGP_MARCH_CS");
-        // default: slabs of ~128-256 cells (measured: C2 nx=512 -> 4 CTAs,
-        // 6.5 us/step; C3 nx=4096 -> 16 CTAs, 9.2 us/step)
+        // default: slabs of >= 64 cells, at most 16 CTAs (measured, latency
+        // mode: C2 nx=512 -> 8 CTAs, 5.5 us/step; C3 nx=4096 -> 16 CTAs,
+        // 9.0 us/step)
         int cs = env > 0 ? env : 16;
         if (env <= 0)
-            while (cs > 1 && nx / cs < 128) cs /= 2;
+            while (cs > 1 && nx / cs < 64) cs /= 2;
         while (cs > 1 && (nx % cs || nx / cs < 64)) cs /= 2;
         return cs;
     }
@@ -855,17 +1022,23 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
       if constexpr (K != 2 || MODEL != MGP_MODEL_BURGERS) {
         return MGP_EINVAL;
       } else {
-        // slabs: P = 8 above 512 cells per CTA, P = 1 (latency) otherwise
-        const bool wide = a.phi.nx / cs > 512;
+        // slabs: P = 8 above 512 cells per CTA; below, the latency mode
+        // (two threads per interface) for slabs <= 256 cells, else P = 1
+        const int64_t nsl = a.phi.nx / cs;
+        const int mode = nsl > 512 ? 8 : (nsl <= 256 ? 0 : 1);
         switch (cs) {
-            case 2: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 2>(a, st)
-                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 2>(a, st);
-            case 4: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 4>(a, st)
-                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 4>(a, st);
-            case 8: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 8>(a, st)
-                                : launch_t<K, REG, MODEL, 1, MGP_REGS, 8>(a, st);
-            case 16: return wide ? launch_t<K, REG, MODEL, 8, MGP_REGS, 16>(a, st)
-                                 : launch_t<K, REG, MODEL, 1, MGP_REGS, 16>(a, st);
+            case 2: return mode == 8 ? launch_t<K, REG, MODEL, 8, MGP_REGS, 2>(a, st)
+                         : mode == 0 ? launch_t<K, REG, MODEL, 0, MGP_REGS, 2>(a, st)
+                                     : launch_t<K, REG, MODEL, 1, MGP_REGS, 2>(a, st);
+            case 4: return mode == 8 ? launch_t<K, REG, MODEL, 8, MGP_REGS, 4>(a, st)
+                         : mode == 0 ? launch_t<K, REG, MODEL, 0, MGP_REGS, 4>(a, st)
+                                     : launch_t<K, REG, MODEL, 1, MGP_REGS, 4>(a, st);
+            case 8: return mode == 8 ? launch_t<K, REG, MODEL, 8, MGP_REGS, 8>(a, st)
+                         : mode == 0 ? launch_t<K, REG, MODEL, 0, MGP_REGS, 8>(a, st)
+                                     : launch_t<K, REG, MODEL, 1, MGP_REGS, 8>(a, st);
+            case 16: return mode == 8 ? launch_t<K, REG, MODEL, 8, MGP_REGS, 16>(a, st)
+                          : mode == 0 ? launch_t<K, REG, MODEL, 0, MGP_REGS, 16>(a, st)
+                                      : launch_t<K, REG, MODEL, 1, MGP_REGS, 16>(a, st);
         }
         return MGP_EINVAL;
       }
@@ -971,6 +1144,18 @@ int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
 }
 
 int64_t mgp_launch_count(void) { return (int64_t)g_launches; }
+
+#ifdef MGP_TRACE
+int mgp_trace_read(long long *out, int n) {
+    int cnt = 0;
+    cudaMemcpyFromSymbol(&cnt, g_trace_n, sizeof(int));
+    if (cnt > n / 2) cnt = n / 2;
+    cudaMemcpyFromSymbol(out, g_trace, sizeof(long long) * 2 * cnt);
+    int zero = 0;
+    cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(int));
+    return cnt;
+}
+#endif
 
 int32_t mgp_sweep_args_layout(int64_t *out, int32_t n) {
 #define MGP_OFF(f) (int64_t) offsetof(mgp_sweep_args, f)
