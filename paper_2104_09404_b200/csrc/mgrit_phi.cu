@@ -128,9 +128,6 @@ constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
 #ifndef MGP_SLIDE_UNROLL
 #define MGP_SLIDE_UNROLL 1
 #endif
-#ifndef MGP_SKEW
-#define MGP_SKEW 0
-#endif
 #define MGP_PRAGMA(x) _Pragma(#x)
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
 #define MGP_UNROLL(n) MGP_UNROLL_(n)
@@ -252,7 +249,8 @@ __device__ __forceinline__ double weno_value_ieee(const double *beta, const doub
 
 template <int K>
 __device__ __forceinline__ double weno_value(const double *beta, const double *q, double eps,
-                                             bool moot = false) {
+                                             const double *moot_win = nullptr,
+                                             bool moot_extra = false) {
     bool bad = false;
     double raw[K + 1];
 #pragma unroll
@@ -267,10 +265,18 @@ __device__ __forceinline__ double weno_value(const double *beta, const double *q
     double v = mgp::div_fast(raw[0], R, bad) * q[0];
 #pragma unroll
     for (int r = 1; r <= K; ++r) v = v + mgp::div_fast(raw[r], R, bad) * q[r];
-    // `moot`: the value cannot reach the result (Burgers with a non-finite
-    // cell in the field: alpha is NaN and every flux NaN), so skip the
-    // slow exact recomputation on such data
-    if (bad && !moot) v = weno_value_ieee<K>(beta, q, eps);
+    if (bad) {
+        // `moot`: the value cannot reach the result (Burgers with a non-finite
+        // cell in the field: alpha is NaN and every flux NaN), so skip the
+        // slow exact recomputation on such data.  Checked only on this rare
+        // path.
+        bool moot = moot_extra;
+        if (moot_win) {
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(moot_win[t]);
+        }
+        if (!moot) v = weno_value_ieee<K>(beta, q, eps);
+    }
     return v;
 }
 
@@ -372,8 +378,7 @@ struct Field {
 #pragma unroll
                 for (int r = 0; r <= K; ++r) q[r] = cand_right<K, REG>(win, r);
             }
-            const bool moot = MODEL == MGP_MODEL_BURGERS && badw;
-            double v = weno_value<K>(b, q, k.eps, moot);
+            double v = weno_value<K>(b, q, k.eps, nullptr, MODEL == MGP_MODEL_BURGERS && badw);
             if (kCheck && badw) v = __longlong_as_double(kNaNBits);
             if (side == 0) s_L[sk(i)] = v;
             else s_R[sk(i)] = v;
@@ -425,71 +430,6 @@ struct Field {
         }
 #pragma unroll
         for (int r = 0; r <= K; ++r) ql[r] = cand_left<K, REG>(win, r);
-#if MGP_SKEW
-        // Skewed pipeline: iteration p forms the products of the left state
-        // at i+1 while finishing the weights of left(i) and right(i-1), whose
-        // inputs are already complete -- two independent division chains
-        // overlap the product/sum work of the next interface.
-        double br_prev[K + 1], qr_prev[K + 1];
-        bool badr_prev = false, moot_prev = false;
-        MGP_UNROLL(MGP_SLIDE_UNROLL)
-        for (int p = 0; p <= n; ++p) {
-            const int i = i0 + p;
-            const bool body = p < n;
-            bool bad_left = false, bad_right = false, moot = false;
-            double bl_next[K + 1], br[K + 1], ql_next[K + 1], qr[K + 1];
-            if (body) {
-                const bool bad_here = !is_finite(win[K]);
-                if (kCheck) {
-#pragma unroll
-                    for (int t = 0; t <= 2 * K; ++t) bad_left |= !is_finite(win[t]);
-                }
-#pragma unroll
-                for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
-                win[2 * K] = cell(i + 1 + K);
-                if (kCheck) {
-#pragma unroll
-                    for (int t = 0; t <= 2 * K; ++t) bad_right |= !is_finite(win[t]);
-                }
-#pragma unroll
-                for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl_next[s], br[K - s]);
-#pragma unroll
-                for (int r = 0; r <= K; ++r) {
-                    ql_next[r] = cand_left<K, REG>(win, r);
-                    qr[r] = cand_right<K, REG>(win, r);
-                }
-                if (MODEL == MGP_MODEL_BURGERS) {
-#pragma unroll
-                    for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(win[t]);
-                    moot |= bad_here;
-                    if (bad_here) m = kNaNBits;
-                }
-                double ul = weno_value<K>(bl, ql, k.eps, moot);
-                if (kCheck && bad_left) ul = __longlong_as_double(kNaNBits);
-                s_L[sk(i)] = ul;
-                if (MODEL == MGP_MODEL_BURGERS) m = umax64(m, abs_bits(ul));
-                if (CS > 1 && i == ns - 1) r_edge_right[0] = ul;
-            }
-            if (p > 0) {
-                double ur = weno_value<K>(br_prev, qr_prev, k.eps, moot_prev);
-                if (kCheck && badr_prev) ur = __longlong_as_double(kNaNBits);
-                s_R[sk(i - 1)] = ur;
-                if (MODEL == MGP_MODEL_BURGERS) m = umax64(m, abs_bits(ur));
-                if (CS > 1 && i - 1 == ns - 1) r_edge_right[1] = ur;
-            }
-            if (body) {
-#pragma unroll
-                for (int s = 0; s <= K; ++s) {
-                    bl[s] = bl_next[s];
-                    ql[s] = ql_next[s];
-                    br_prev[s] = br[s];
-                    qr_prev[s] = qr[s];
-                }
-                badr_prev = bad_right;
-                moot_prev = moot;
-            }
-        }
-#else
         MGP_UNROLL(MGP_SLIDE_UNROLL)
         for (int p = 0; p < n; ++p) {
             const int i = i0 + p;
@@ -518,14 +458,9 @@ struct Field {
                 ql_next[r] = cand_left<K, REG>(win, r);
                 qr[r] = cand_right<K, REG>(win, r);
             }
-            bool moot = false;
-            if (MODEL == MGP_MODEL_BURGERS) {
-#pragma unroll
-                for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(win[t]);
-                moot |= bad_here;
-            }
-            double ul = weno_value<K>(bl, ql, k.eps, moot);
-            double ur = weno_value<K>(br, qr, k.eps, moot);
+            const bool burg = MODEL == MGP_MODEL_BURGERS;
+            double ul = weno_value<K>(bl, ql, k.eps, burg ? win : nullptr, burg && bad_here);
+            double ur = weno_value<K>(br, qr, k.eps, burg ? win : nullptr, burg && bad_here);
             if (kCheck) {
                 if (bad_left) ul = __longlong_as_double(kNaNBits);
                 if (bad_right) ur = __longlong_as_double(kNaNBits);
@@ -546,7 +481,6 @@ struct Field {
                 ql[s] = ql_next[s];
             }
         }
-#endif
         return m;
     }
 
