@@ -55,6 +55,11 @@ extern "C" {
 #define MGP_SUM_SEQ 0
 #define MGP_SUM_LANE2 1
 
+/* propagator family (mgp_phi.scheme) */
+#define MGP_SCHEME_RK_WENO 0     /* RungeKuttaStepper over WENO + global LF (stepper.py:68-82) */
+#define MGP_SCHEME_LF_ONESTEP 1  /* MatchedLFFine / RediscretizedLF (stepper.py:102-114,155-167) */
+#define MGP_SCHEME_LF_MATCHED 2  /* MatchedLFCoarse order 0/1 (stepper.py:117-152) */
+
 /* how "+ g" is applied after a propagator application */
 #define MGP_G_NONE 0   /* no addition (advance, serial march)              */
 #define MGP_G_ZERO 1   /* + 0.0 (finest-level g, zero past node 0)         */
@@ -71,7 +76,10 @@ extern "C" {
 
 /* One propagator Phi_l: SSP-RK(rk_order) over the WENO(2k+1)/global-LF
  * semi-discrete operator on a periodic mesh of nx cells
- * (harness.py:350-355 builds one per level with dt = dt0 * m**l). */
+ * (harness.py:350-355 builds one per level with dt = dt0 * m**l), or a
+ * member of the one-step Lax-Friedrichs family (scheme != 0; Burgers, nx <=
+ * 2048; dt is the step the formula multiplies: dt for one-step and matched
+ * order 0 (= dt_fine * m_eff), dt_fine for matched order 1). */
 typedef struct mgp_phi {
     int32_t model;      /* MGP_MODEL_*                                        */
     int32_t weno_k;     /* reconstruction degree 0..3 (order 2k+1), flux.py:35 */
@@ -82,6 +90,11 @@ typedef struct mgp_phi {
     double dx;          /* SpatialGrid.dx = length / nx (grid.py:35-37)        */
     double epsilon;     /* WENO epsilon > 0 (weno.py:30)                       */
     double speed;       /* advection speed a (ignored for Burgers)             */
+    int32_t scheme;     /* MGP_SCHEME_* (0 for the WENO/RK propagators)        */
+    int32_t lf_order;   /* MGP_SCHEME_LF_MATCHED: truncation order 0 or 1      */
+    int32_t m_eff;      /* MGP_SCHEME_LF_MATCHED: fine steps emulated (m^l)    */
+    int32_t repeats;    /* >= 1: Phi = inner^repeats (ComposedStepper,
+                           stepper.py:170-188); 1 otherwise                    */
 } mgp_phi;
 
 /*

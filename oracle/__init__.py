@@ -37,7 +37,9 @@ class OraParams(ctypes.Structure):
     _fields_ = [("model", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("rk_order", ctypes.c_int32), ("regime", ctypes.c_int32),
                 ("dt", ctypes.c_double), ("dx", ctypes.c_double),
-                ("eps", ctypes.c_double), ("speed", ctypes.c_double)]
+                ("eps", ctypes.c_double), ("speed", ctypes.c_double),
+                ("scheme", ctypes.c_int32), ("lf_order", ctypes.c_int32),
+                ("m_eff", ctypes.c_int32), ("repeats", ctypes.c_int32)]
 
 
 _lib = None
@@ -78,10 +80,16 @@ def _ptr(a):
 
 
 def make_params(*, model="burgers", k=2, rk_order=3, dt=1e-3, dx=1.0 / 64,
-                eps=1e-6, speed=1.0, regime=SUM_SEQ) -> OraParams:
+                eps=1e-6, speed=1.0, regime=SUM_SEQ, scheme=0, lf_order=0, m_eff=1,
+                repeats=1) -> OraParams:
+    """scheme 0: RK over WENO/LF; 1: one-step LF (matched-lf-fine,
+    rediscretized-lf), 2: matched coarse LF of order lf_order emulating m_eff
+    fine steps (dt = the step the formula multiplies, see include/mgrit_phi.h);
+    repeats: ComposedStepper count."""
     m = MODEL_BURGERS if model == "burgers" else MODEL_ADVECTION
     return OraParams(m, int(k), int(rk_order), int(regime), float(dt),
-                     float(dx), float(eps), float(speed))
+                     float(dx), float(eps), float(speed), int(scheme), int(lf_order),
+                     int(m_eff), int(repeats))
 
 
 def regime_for_shape(shape) -> int:
@@ -139,15 +147,20 @@ class OracleStepper:
     follows the shape of u exactly as NumPy does in the reference."""
 
     def __init__(self, *, model="burgers", k=2, rk_order=3, dt, dx,
-                 eps=1e-6, speed=1.0, nthreads=0):
+                 eps=1e-6, speed=1.0, nthreads=0, scheme=0, lf_order=0, m_eff=1,
+                 repeats=1, formula_dt=None):
         self.model, self.k, self.order = model, k, rk_order
         self.dt, self.dx, self.eps, self.speed = dt, dx, eps, speed
         self.nthreads = nthreads
+        self.scheme, self.lf_order, self.m_eff, self.repeats = scheme, lf_order, m_eff, repeats
+        self.formula_dt = dt if formula_dt is None else formula_dt
 
     def params(self, regime: int) -> OraParams:
         return make_params(model=self.model, k=self.k, rk_order=self.order,
-                           dt=self.dt, dx=self.dx, eps=self.eps,
-                           speed=self.speed, regime=regime)
+                           dt=self.formula_dt, dx=self.dx, eps=self.eps,
+                           speed=self.speed, regime=regime, scheme=self.scheme,
+                           lf_order=self.lf_order, m_eff=self.m_eff,
+                           repeats=self.repeats)
 
     def advance(self, u):
         u = np.asarray(u, dtype=np.float64)

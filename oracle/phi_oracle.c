@@ -52,6 +52,10 @@ typedef struct {
     int32_t rk_order;  /* 1 FE, 2 SSP-RK2, 3 SSP-RK3; 0 = semi-discrete rhs  */
     int32_t regime;    /* ORA_SUM_SEQ / ORA_SUM_LANE2                        */
     double dt, dx, eps, speed;
+    int32_t scheme;    /* 0 RK/WENO, 1 one-step LF, 2 matched LF (coarse)    */
+    int32_t lf_order;  /* matched: 0 or 1                                     */
+    int32_t m_eff;     /* matched: fine steps emulated                        */
+    int32_t repeats;   /* composition count (ComposedStepper), >= 1           */
 } ora_params;
 
 /* ---- exact rational tables, weno.py:43-86.  IEEE division of the small
@@ -153,20 +157,21 @@ static double recon(const ora_tables *t, int regime, const double *w) {
 typedef struct {
     int64_t nx;
     double *pad;   /* field with k+1 periodic halo cells on both sides */
-    double *ul, *ur, *F, *A, *u1, *u2;
+    double *ul, *ur, *F, *A, *u1, *u2, *tmp;
 } ora_work;
 
 static int work_alloc(ora_work *w, int64_t nx, int k) {
     w->nx = nx;
     const int64_t H = k + 1;
     w->pad = (double *)malloc(sizeof(double) * (size_t)(nx + 2 * H));
-    w->ul = (double *)malloc(sizeof(double) * (size_t)nx * 6);
+    w->ul = (double *)malloc(sizeof(double) * (size_t)nx * 7);
     if (!w->pad || !w->ul) { free(w->pad); free(w->ul); return 1; }
     w->ur = w->ul + nx;
     w->F = w->ur + nx;
     w->A = w->F + nx;
     w->u1 = w->A + nx;
     w->u2 = w->u1 + nx;
+    w->tmp = w->u2 + nx;
     return 0;
 }
 
@@ -221,11 +226,80 @@ static void rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
     }
 }
 
+/* E(u)_i = 0.5 (u_{i+1} + u_{i-1})  (stepper.py:85-87) */
+static void ora_E(const double *u, double *out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = 0.5 * (u[i + 1 == n ? 0 : i + 1] + u[i == 0 ? n - 1 : i - 1]);
+}
+
+/* D(f)_i = (f_{i+1} - f_{i-1}) / (2 dx)  (stepper.py:90-92) */
+static void ora_D(const double *f, double dx, double *out, int64_t n) {
+    const double twodx = 2.0 * dx;
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = (f[i + 1 == n ? 0 : i + 1] - f[i == 0 ? n - 1 : i - 1]) / twodx;
+}
+
+/* MatchedLFFine / RediscretizedLF (stepper.py:102-114,155-167) and
+ * MatchedLFCoarse (stepper.py:117-152); Burgers flux (0.5 u) u. */
+static void lf_field(const ora_params *p, ora_work *wk, const double *u, double *out) {
+    const int64_t n = wk->nx;
+    double *f = wk->ul, *d = wk->ur, *v = wk->F, *v2 = wk->A, *acc = wk->u1, *e = wk->u2;
+    for (int64_t i = 0; i < n; ++i) f[i] = (0.5 * u[i]) * u[i];
+    if (p->scheme == 1) {
+        ora_E(u, v, n);
+        ora_D(f, p->dx, d, n);
+        for (int64_t i = 0; i < n; ++i) out[i] = v[i] - (p->dt * d[i]);
+        return;
+    }
+    if (p->lf_order == 0) {
+        memcpy(v, u, sizeof(double) * (size_t)n);
+        for (int j = 0; j < p->m_eff; ++j) {
+            ora_E(v, v2, n);
+            memcpy(v, v2, sizeof(double) * (size_t)n);
+        }
+        ora_D(f, p->dx, d, n);
+        for (int64_t i = 0; i < n; ++i) out[i] = v[i] - (p->dt * d[i]);
+        return;
+    }
+    ora_D(f, p->dx, acc, n);
+    memcpy(v, u, sizeof(double) * (size_t)n);
+    for (int j = 0; j < p->m_eff - 1; ++j) {
+        ora_E(v, v2, n);
+        memcpy(v, v2, sizeof(double) * (size_t)n);
+        for (int64_t i = 0; i < n; ++i) f[i] = (0.5 * v[i]) * v[i];
+        ora_E(acc, e, n);
+        ora_D(f, p->dx, d, n);
+        for (int64_t i = 0; i < n; ++i) acc[i] = e[i] + d[i];
+    }
+    ora_E(v, v2, n);
+    for (int64_t i = 0; i < n; ++i) out[i] = v2[i] - (p->dt * acc[i]);
+}
+
 /* RungeKuttaStepper.advance (stepper.py:50-82) + optional relaxation "+ g" */
+static void phi_once(const ora_params *p, const ora_tables *t, ora_work *wk,
+                     const double *u, double *out);
+
+/* ComposedStepper (stepper.py:170-188): inner^repeats, then "+ g" */
 static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
                       const double *u, const double *g, double *out) {
     const int64_t nx = wk->nx;
+    phi_once(p, t, wk, u, out);
+    for (int r = 1; r < p->repeats; ++r) {
+        memcpy(wk->tmp, out, sizeof(double) * (size_t)nx);
+        phi_once(p, t, wk, wk->tmp, out);
+    }
+    if (g)
+        for (int64_t i = 0; i < nx; ++i) out[i] = out[i] + g[i];
+}
+
+static void phi_once(const ora_params *p, const ora_tables *t, ora_work *wk,
+                     const double *u, double *out) {
+    const int64_t nx = wk->nx;
     double *A = wk->A, *u1 = wk->u1, *u2 = wk->u2;
+    if (p->scheme != 0) {
+        lf_field(p, wk, u, out);
+        return;
+    }
     if (p->rk_order == 0) {
         rhs_field(p, t, wk, u, out);
         return;
@@ -251,12 +325,15 @@ static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
         for (int64_t i = 0; i < nx; ++i)
             out[i] = ((u[i] / 3.0) + (two3 * u2[i])) + (tdt * A[i]);
     }
-    if (g)
-        for (int64_t i = 0; i < nx; ++i) out[i] = out[i] + g[i];
 }
 
 static int check_params(const ora_params *p, int64_t nx) {
-    if (!p || p->k < 0 || p->k > 3) return 1;
+    if (!p || p->repeats < 1) return 1;
+    if (p->scheme == 1 || p->scheme == 2)
+        return (p->model != ORA_MODEL_BURGERS || nx < 1 ||
+                (p->scheme == 2 && (p->m_eff < 1 || p->lf_order < 0 || p->lf_order > 1)));
+    if (p->scheme != 0) return 1;
+    if (p->k < 0 || p->k > 3) return 1;
     if (p->rk_order < 0 || p->rk_order > 3) return 1;
     if (p->model != ORA_MODEL_BURGERS && p->model != ORA_MODEL_ADVECTION) return 1;
     if (p->regime != ORA_SUM_SEQ && p->regime != ORA_SUM_LANE2) return 1;

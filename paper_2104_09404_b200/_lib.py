@@ -25,6 +25,7 @@ MGP_OK, MGP_EINVAL, MGP_ECUDA = 0, 1, 2
 SUM_SEQ, SUM_LANE2 = 0, 1
 G_NONE, G_ZERO, G_ARRAY = 0, 1, 2
 TAIL_NONE, TAIL_PHI, TAIL_RESTRICT, TAIL_RESID = 0, 1, 2, 3
+SCHEME_RK_WENO, SCHEME_LF_ONESTEP, SCHEME_LF_MATCHED = 0, 1, 2
 GUESS_LAST_STEP, GUESS_INJECTION = 0, 1
 
 NVCC_FLAGS = [
@@ -42,7 +43,9 @@ class MgpPhi(ctypes.Structure):
                 ("rk_order", ctypes.c_int32), ("regime", ctypes.c_int32),
                 ("nx", ctypes.c_int64), ("dt", ctypes.c_double),
                 ("dx", ctypes.c_double), ("epsilon", ctypes.c_double),
-                ("speed", ctypes.c_double)]
+                ("speed", ctypes.c_double), ("scheme", ctypes.c_int32),
+                ("lf_order", ctypes.c_int32), ("m_eff", ctypes.c_int32),
+                ("repeats", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p

@@ -283,7 +283,9 @@ __device__ __forceinline__ double weno_value(const double *beta, const double *q
 struct Consts {
     double dt, hdt, qdt, tdt, two3, inv_dx, dx, eps, speed, half_alpha_adv;
     double k0_omega;
-    int dx_pow2;
+    double twodx, inv_twodx;   // one-step LF family: central difference 2 dx
+    int dx_pow2, twodx_pow2;
+    int lf_order, m_eff;
 };
 
 namespace cg = cooperative_groups;
@@ -331,7 +333,10 @@ struct Field {
     // 1.8-2.5x slower per stage on B200)
     __device__ __forceinline__ void sync() { field_sync<CS>(); }
 
+    static constexpr int HALO = H;
     __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
+    __device__ __forceinline__ void load(int t, double v) { s_u[sk(t + H)] = v; }
+    __device__ __forceinline__ double result(int t) const { return s_R[sk(t)]; }
     __device__ __forceinline__ void put(int t, double v) {
         s_u[sk(t + H)] = v;
         if (CS == 1) {
@@ -623,35 +628,14 @@ __device__ __forceinline__ double g_value(int mode, const double *g, int c) {
     return mode == MGP_G_ARRAY ? g[c] : 0.0;
 }
 
-template <int K, int REG, int MODEL, int P, int REGS, int CS>
-__global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
-    extern __shared__ double smem[];
-    using F = Field<K, REG, MODEL, P, CS>;
-    F f;
+// The sweep over chunks (mgp_sweep semantics, include/mgrit_phi.h), generic
+// over the propagator held in shared memory (WENO/RK Field or LFField).
+template <class F, int CS>
+__device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts &k, F &f,
+                                           const int ns, const int q, const int c0,
+                                           double *s_sum, double *s_psum) {
     const int nx = (int)a.phi.nx;
-    const int ns = nx / CS;            // cells of this CTA's slab
-    const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
-    const int c0 = q * ns;             // global index of local cell 0
     const int tid = threadIdx.x, nt = blockDim.x;
-    f.ns = ns;
-    f.q = q;
-    f.run = tid;
-    f.i0 = tid * F::PC;
-    f.s_u = smem;
-    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
-    f.s_R = f.s_L + sk_size(ns);
-    f.s_u0 = f.s_R + sk_size(ns);
-    double *s_sum = f.s_u0 + sk_size(ns);      // [3 * 32]
-    double *s_psum = s_sum + 3 * 32;           // [3 * CS] cluster partials
-    f.s_edge = s_psum + 3 * CS;                // [2]
-    f.s_cmax = reinterpret_cast<unsigned long long *>(f.s_edge + 2);   // [CS]
-    f.s_red = f.s_cmax + CS;                   // [32]
-    if (CS > 1) {
-        cg::cluster_group cl = cg::this_cluster();
-        f.r_u_left = cl.map_shared_rank(f.s_u, (q + CS - 1) % CS);
-        f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
-        f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
-    }
     const int rk = a.phi.rk_order;
     const int total = a.n_steps + (a.tail != MGP_TAIL_NONE ? 1 : 0);
     const int64_t first = blockIdx.x / CS, stride = gridDim.x / CS;
@@ -661,11 +645,11 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
         const double *x0 = a.start + b * a.start_stride;
         const double *ref = a.ref ? a.ref + b * a.ref_cs : nullptr;
         // slab and halo straight from global memory (periodic)
-        for (int t = tid - F::H; t < ns + F::H; t += nt) {
+        for (int t = tid - F::HALO; t < ns + F::HALO; t += nt) {
             int c = c0 + t;
             c = c < 0 ? c + nx : (c >= nx ? c - nx : c);
             const double v = x0[c];
-            f.s_u[sk(t + F::H)] = v;
+            f.load(t, v);
             if (t >= 0 && t < ns) {
                 if (ref) {
                     const double d = v - ref[c];
@@ -677,14 +661,21 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
         for (int s = 1; s <= total; ++s) {
             f.sync();  // s_u and halos complete
             f.phi(k, rk);
-            __syncthreads();   // results in s_R complete
+            __syncthreads();   // results complete
+            // ComposedStepper (stepper.py:170-188): Phi = inner^repeats
+            for (int rep = 1; rep < a.phi.repeats; ++rep) {
+                for (int t = tid; t < ns; t += nt) f.put(t, f.result(t));
+                f.sync();
+                f.phi(k, rk);
+                __syncthreads();
+            }
             if (s <= a.n_steps) {
                 const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
                 double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
                 const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
                 for (int t = tid; t < ns; t += nt) {
                     const int c = c0 + t;
-                    const double v = add_g(f.s_R[sk(t)], a.g_mode, g, c);
+                    const double v = add_g(f.result(t), a.g_mode, g, c);
                     f.put(t, v);
                     if (st) st[c] = v;
                     if (rs) {
@@ -699,7 +690,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
             if (a.tail == MGP_TAIL_PHI) {
                 double *out = a.tail_out + b * a.to_s;
                 for (int t = tid; t < ns; t += nt)
-                    out[c0 + t] = add_g(f.s_R[sk(t)], a.tail_g_mode, tg, c0 + t);
+                    out[c0 + t] = add_g(f.result(t), a.tail_g_mode, tg, c0 + t);
             } else if (a.tail == MGP_TAIL_RESTRICT) {
                 // mgrit.py:211-215: g_c = (g_f + phi) - psi;
                 // u_c = phi + g_f (last-step) or u_f (injection)
@@ -712,7 +703,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                     const double p = phi[c];
                     const double left =
                         (a.tail_g_mode == MGP_G_NONE) ? p : g_value(a.tail_g_mode, tg, c) + p;
-                    gc[c] = left - f.s_R[sk(t)];
+                    gc[c] = left - f.result(t);
                     uc[c] = (a.guess == MGP_GUESS_LAST_STEP) ? add_g(p, a.tail_g_mode, tg, c)
                                                              : uf[c];
                 }
@@ -722,7 +713,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
                 const double *rn = (last && a.ref) ? a.ref + (b + 1) * a.ref_cs : nullptr;
                 for (int t = tid; t < ns; t += nt) {
                     const int c = c0 + t;
-                    const double y = f.s_R[sk(t)];
+                    const double y = f.result(t);
                     const double pred =
                         (a.tail_g_mode == MGP_G_NONE) ? y : g_value(a.tail_g_mode, tg, c) + y;
                     const double u = tgt[c];
@@ -777,6 +768,132 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     }
 }
 
+template <int K, int REG, int MODEL, int P, int REGS, int CS>
+__global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
+    extern __shared__ double smem[];
+    using F = Field<K, REG, MODEL, P, CS>;
+    F f;
+    const int nx = (int)a.phi.nx;
+    const int ns = nx / CS;            // cells of this CTA's slab
+    const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
+    const int c0 = q * ns;             // global index of local cell 0
+    const int tid = threadIdx.x, nt = blockDim.x;
+    f.ns = ns;
+    f.q = q;
+    f.run = tid;
+    f.i0 = tid * F::PC;
+    f.s_u = smem;
+    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
+    f.s_R = f.s_L + sk_size(ns);
+    f.s_u0 = f.s_R + sk_size(ns);
+    double *s_sum = f.s_u0 + sk_size(ns);      // [3 * 32]
+    double *s_psum = s_sum + 3 * 32;           // [3 * CS] cluster partials
+    f.s_edge = s_psum + 3 * CS;                // [2]
+    f.s_cmax = reinterpret_cast<unsigned long long *>(f.s_edge + 2);   // [CS]
+    f.s_red = f.s_cmax + CS;                   // [32]
+    if (CS > 1) {
+        cg::cluster_group cl = cg::this_cluster();
+        f.r_u_left = cl.map_shared_rank(f.s_u, (q + CS - 1) % CS);
+        f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
+        f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
+    }
+    sweep_body<F, CS>(a, k, f, ns, q, c0, s_sum, s_psum);
+}
+
+// ---------------------------------------------------------------------------
+// One-step Lax-Friedrichs family (stepper.py:85-167), Burgers only:
+//   E(u)_i = 0.5 (u_{i+1} + u_{i-1}),  D(f)_i = (f_{i+1} - f_{i-1}) / (2 dx)
+//   one-step (matched-lf-fine, rediscretized-lf):  Phi(u) = E u - dt D f(u)
+//   matched order 0:  E^m u - (m dt) D f(u)
+//   matched order 1:  acc = D f(u); v = u; m-1 times { v = E v;
+//                     acc = E acc + D f(v) };  Phi(u) = E v - dt_fine acc
+// Elementwise NumPy arithmetic: no summation-order subtleties.  The whole
+// field lives in shared memory (nx <= kMaxLfNx); one CTA per chunk.
+// ---------------------------------------------------------------------------
+constexpr int kMaxLfNx = 2048;
+
+template <int MODE>   // 1 = one-step, 2 = matched coarse
+struct LFField {
+    static constexpr int HALO = 0;
+    int ns;
+    double *s_u, *s_R, *s_va, *s_vb, *s_aa, *s_ab, *s_f;
+
+    __device__ __forceinline__ void load(int t, double v) {
+        if (t >= 0 && t < ns) s_u[t] = v;
+    }
+    __device__ __forceinline__ void put(int t, double v) { s_u[t] = v; }
+    __device__ __forceinline__ double result(int t) const { return s_R[t]; }
+    __device__ __forceinline__ void sync() { __syncthreads(); }
+    __device__ __forceinline__ int up(int c) const { return c + 1 == ns ? 0 : c + 1; }
+    __device__ __forceinline__ int dn(int c) const { return c == 0 ? ns - 1 : c - 1; }
+    __device__ __forceinline__ double E(const double *v, int c) const {
+        return 0.5 * (v[up(c)] + v[dn(c)]);
+    }
+    __device__ __forceinline__ double D(const Consts &k, const double *f, int c) const {
+        const double d = f[up(c)] - f[dn(c)];
+        return k.twodx_pow2 ? d * k.inv_twodx : d / k.twodx;
+    }
+
+    __device__ void phi(const Consts &k, int) {
+        const int tid = threadIdx.x, nt = blockDim.x;
+        for (int c = tid; c < ns; c += nt) s_f[c] = (0.5 * s_u[c]) * s_u[c];
+        __syncthreads();
+        if (MODE == 1) {
+            for (int c = tid; c < ns; c += nt) s_R[c] = E(s_u, c) - (k.dt * D(k, s_f, c));
+            return;
+        }
+        if (k.lf_order == 0) {
+            const double *src = s_u;
+            double *dst = s_va;
+            for (int j = 0; j < k.m_eff; ++j) {
+                for (int c = tid; c < ns; c += nt) dst[c] = E(src, c);
+                __syncthreads();
+                src = dst;
+                dst = (dst == s_va) ? s_vb : s_va;
+            }
+            for (int c = tid; c < ns; c += nt) s_R[c] = src[c] - (k.dt * D(k, s_f, c));
+            return;
+        }
+        double *acc = s_aa, *accn = s_ab;
+        for (int c = tid; c < ns; c += nt) acc[c] = D(k, s_f, c);
+        __syncthreads();
+        const double *v = s_u;
+        double *vn = s_va;
+        for (int j = 0; j < k.m_eff - 1; ++j) {
+            for (int c = tid; c < ns; c += nt) vn[c] = E(v, c);
+            __syncthreads();
+            for (int c = tid; c < ns; c += nt) s_f[c] = (0.5 * vn[c]) * vn[c];
+            __syncthreads();
+            for (int c = tid; c < ns; c += nt) accn[c] = E(acc, c) + D(k, s_f, c);
+            __syncthreads();
+            v = vn;
+            vn = (vn == s_va) ? s_vb : s_va;
+            double *t = acc;
+            acc = accn;
+            accn = t;
+        }
+        for (int c = tid; c < ns; c += nt) s_R[c] = E(v, c) - (k.dt * acc[c]);
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) lf_kernel(const mgp_sweep_args a, const Consts k) {
+    extern __shared__ double smem[];
+    LFField<MODE> f;
+    const int nx = (int)a.phi.nx;
+    f.ns = nx;
+    f.s_u = smem;
+    f.s_R = f.s_u + nx;
+    f.s_va = f.s_R + nx;
+    f.s_vb = f.s_va + nx;
+    f.s_aa = f.s_vb + nx;
+    f.s_ab = f.s_aa + nx;
+    f.s_f = f.s_ab + nx;
+    double *s_sum = f.s_f + nx;
+    double *s_psum = s_sum + 3 * 32;
+    sweep_body<LFField<MODE>, 1>(a, k, f, nx, 0, 0, s_sum, s_psum);
+}
+
 __global__ void __launch_bounds__(1024, 1)
     sum_partials_kernel(const double *p, int64_t n, int width, double *out) {
     __shared__ double s[1024];
@@ -821,6 +938,11 @@ Consts make_consts(const mgp_phi &p) {
     k.half_alpha_adv = 0.5 * (p.speed < 0 ? -p.speed : p.speed);
     const double raw = 1.0 / (p.epsilon * p.epsilon);
     k.k0_omega = raw / raw;
+    k.twodx = 2.0 * p.dx;
+    k.inv_twodx = 1.0 / k.twodx;
+    k.twodx_pow2 = pow2_normal(k.twodx);
+    k.lf_order = p.lf_order;
+    k.m_eff = p.m_eff;
     return k;
 }
 
@@ -1002,6 +1124,27 @@ int launch_m(const mgp_sweep_args &a, cudaStream_t st) {
     return MGP_EINVAL;
 }
 
+template <int MODE>
+int launch_lf(const mgp_sweep_args &a, cudaStream_t st) {
+    const int64_t nx = a.phi.nx;
+    int nt = (int)((nx + 31) / 32 * 32);
+    if (nt > 256) nt = 256;
+    const size_t sm = sizeof(double) * (size_t)(7 * nx + 3 * 32 + 3);
+    auto kern = lf_kernel<MODE>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024) != cudaSuccess)
+            return MGP_ECUDA;
+        attr_set = true;
+    }
+    int64_t grid = a.n_chunks;
+    if (grid > (int64_t)1 << 30) grid = (int64_t)1 << 30;
+    kern<<<(unsigned)grid, nt, sm, st>>>(a, make_consts(a.phi));
+    ++g_launches;
+    return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
+}
+
 int64_t max_nx_for(int k, int model) {
     return (k == 2 && model == MGP_MODEL_BURGERS) ? 16 * kMaxNx : kMaxNx;
 }
@@ -1009,6 +1152,25 @@ int64_t max_nx_for(int k, int model) {
 int validate(const mgp_sweep_args *a) {
     if (!a) return MGP_EINVAL;
     const mgp_phi &p = a->phi;
+    if (p.repeats < 1) return MGP_EINVAL;
+    if (p.scheme != MGP_SCHEME_RK_WENO) {
+        if (p.scheme != MGP_SCHEME_LF_ONESTEP && p.scheme != MGP_SCHEME_LF_MATCHED)
+            return MGP_EINVAL;
+        if (p.model != MGP_MODEL_BURGERS) return MGP_EINVAL;   // stepper.py:95-99
+        if (p.nx < 1 || p.nx > kMaxLfNx || !(p.dx > 0.0)) return MGP_EINVAL;
+        if (p.scheme == MGP_SCHEME_LF_MATCHED &&
+            ((p.lf_order != 0 && p.lf_order != 1) || p.m_eff < 1))
+            return MGP_EINVAL;
+        if (a->n_chunks < 0 || a->n_steps < 0 || !a->start) return MGP_EINVAL;
+        if (a->g_mode == MGP_G_ARRAY && !a->g && a->n_steps > 0) return MGP_EINVAL;
+        if (a->tail == MGP_TAIL_PHI && !a->tail_out) return MGP_EINVAL;
+        if (a->tail == MGP_TAIL_RESTRICT && (!a->tail_out || !a->tail_out2 || !a->aux))
+            return MGP_EINVAL;
+        if (a->tail == MGP_TAIL_RESTRICT && a->guess == MGP_GUESS_INJECTION && !a->aux2)
+            return MGP_EINVAL;
+        if (a->tail == MGP_TAIL_RESID && (!a->aux || !a->partials)) return MGP_EINVAL;
+        return MGP_OK;
+    }
     if (p.model != MGP_MODEL_BURGERS && p.model != MGP_MODEL_ADVECTION) return MGP_EINVAL;
     if (p.weno_k < 0 || p.weno_k > 3) return MGP_EINVAL;
     if (p.rk_order < 0 || p.rk_order > 3) return MGP_EINVAL;
@@ -1053,6 +1215,8 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (rc != MGP_OK) return rc;
     if (args->n_chunks == 0) return MGP_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (args->phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(*args, st);
+    if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
     if (args->phi.model == MGP_MODEL_BURGERS) return launch_m<MGP_MODEL_BURGERS>(*args, st);
     return launch_m<MGP_MODEL_ADVECTION>(*args, st);
 }

@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import device as dev
-from ._lib import MgpPhi, TAIL_PHI
+from ._lib import MgpPhi, SCHEME_RK_WENO, TAIL_PHI
 from .errors import ConfigError, DimensionError
 from .grid import SpatialGrid
 from .models import ConservationModel
@@ -81,7 +81,8 @@ class SemiDiscreteOperator:
         return MgpPhi(int(self.model.abi_model), int(self.config.weno.degree),
                       int(rk_order), int(regime), int(self.space_grid.n_cells),
                       float(dt), float(self.space_grid.dx),
-                      float(self.config.weno.epsilon), float(self.model.speed))
+                      float(self.config.weno.epsilon), float(self.model.speed),
+                      SCHEME_RK_WENO, 0, 0, 1)
 
     def rhs(self, field_):
         """SemiDiscreteOperator.rhs (flux.py:159-161) on the GPU.  Returns the
@@ -91,18 +92,25 @@ class SemiDiscreteOperator:
 
 def apply_phi(op: SemiDiscreteOperator, dt: float, rk_order: int, u):
     """Phi (or the rhs for rk_order 0) on every (1, N) field of u."""
+    return apply_phi_struct(lambda regime: op.phi_struct(dt=dt, rk_order=rk_order,
+                                                         regime=regime),
+                            op.space_grid.n_cells, u)
+
+
+def apply_phi_struct(make_phi, nx: int, u):
+    """Run the propagator built by ``make_phi(regime)`` on every (1, N) field
+    of u (regime = NumPy's summation order for that batch size)."""
     is_tensor = torch.is_tensor(u)
     x = dev.to_device(u)
-    nx = op.space_grid.n_cells
     if x.dim() < 2 or x.shape[-1] != nx or x.shape[-2] != 1:
         raise DimensionError(f"expected (..., 1, {nx}) states, got {tuple(x.shape)}")
     batch = x.numel() // nx
     out = torch.empty_like(x)
     if batch:
         regime = dev.regime_for_batch(batch)
-        dev.sweep(op.phi_struct(dt=dt, rk_order=rk_order, regime=regime),
-                  n_chunks=batch, start=x, start_stride=nx, tail=TAIL_PHI,
-                  tail_regime=regime, tail_out=out, to_s=nx, what="advance")
+        dev.sweep(make_phi(regime), n_chunks=batch, start=x, start_stride=nx,
+                  tail=TAIL_PHI, tail_regime=regime, tail_out=out, to_s=nx,
+                  what="advance")
     if is_tensor:
         return out
     return out.cpu().numpy()

@@ -25,7 +25,8 @@ from .flux import FluxConfig, SemiDiscreteOperator, WenoConfig
 from .grid import SpatialGrid, TemporalGrid
 from .models import make_model
 from .serial import discretise_ic
-from .stepper import RungeKuttaStepper
+from .stepper import (ComposedStepper, MatchedLFCoarse, MatchedLFFine,
+                      RediscretizedLF, RungeKuttaStepper)
 from .weno import DEFAULT_EPSILON
 
 _RK_ORDER = {"fe": 1, "ssprk2": 2, "ssprk3": 3}
@@ -36,17 +37,42 @@ def _expand(per_level, n_levels: int) -> tuple:
     return per_level * n_levels if len(per_level) == 1 else per_level
 
 
+COARSE_KINDS = ("rediscretize", "matched-0", "matched-1", "exact")
+
+
 def build_steppers(model, space_grid: SpatialGrid, time_grid: TemporalGrid, *,
                    n_levels: int, m: int, weno_order=(1,), stepper=("fe",),
-                   epsilon: float = DEFAULT_EPSILON, flux: str = "lf") -> list:
-    """One GPU propagator per level, finest first (harness.py:324-356)."""
+                   epsilon: float = DEFAULT_EPSILON, flux: str = "lf",
+                   coarse: str = "rediscretize") -> list:
+    """One GPU propagator per level, finest first (harness.py:324-356):
+    stepper ("matched-lf",) builds the one-step LF family with the coarse
+    operator named by ``coarse``; Runge-Kutta kinds rediscretise per level,
+    or compose the fine step exactly for ``coarse = "exact"``."""
+    if coarse not in COARSE_KINDS:
+        raise ConfigError(f"unknown coarse operator '{coarse}'")
+    dt0 = time_grid.dt
+    if tuple(stepper) == ("matched-lf",):
+        fine = MatchedLFFine(model, space_grid, dt0)
+        out = [fine]
+        for l in range(1, n_levels):
+            m_eff = m ** l
+            if coarse == "exact":
+                out.append(ComposedStepper(fine, m_eff))
+            elif coarse == "rediscretize":
+                out.append(RediscretizedLF(model, space_grid, dt0 * m_eff))
+            else:
+                out.append(MatchedLFCoarse(model, space_grid, dt0, m_eff,
+                                           0 if coarse == "matched-0" else 1))
+        return out
     kinds = _expand(stepper, n_levels)
     orders = _expand(weno_order, n_levels)
     if len(kinds) != n_levels or len(orders) != n_levels:
         raise ConfigError("per-level lists must have one entry or n_levels entries")
-    dt0 = time_grid.dt
     out = []
     for l in range(n_levels):
+        if l > 0 and coarse == "exact":
+            out.append(ComposedStepper(out[0], m ** l))
+            continue
         if kinds[l] not in _RK_ORDER:
             raise ConfigError(f"stepper '{kinds[l]}' is not on the B200 path")
         op = SemiDiscreteOperator(model, space_grid,
@@ -125,6 +151,7 @@ class Problem:
     residual_tol: float | None = None
     epsilon: float = DEFAULT_EPSILON
     length: float = 1.0
+    coarse: str = "rediscretize"
 
     def scaled(self, **kw) -> "Problem":
         return replace(self, **kw)
@@ -152,7 +179,7 @@ class Problem:
         return build_steppers(self.model_obj(), self.space_grid(), tg,
                               n_levels=self.n_levels, m=self.m,
                               weno_order=self.weno_order, stepper=self.stepper,
-                              epsilon=self.epsilon)
+                              epsilon=self.epsilon, coarse=self.coarse)
 
     def options(self):
         from .mgrit import MgritOptions

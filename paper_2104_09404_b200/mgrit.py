@@ -41,7 +41,7 @@ from ._lib import (G_ARRAY, G_NONE, G_ZERO, GUESS_INJECTION, GUESS_LAST_STEP,
                    SUM_SEQ, TAIL_NONE, TAIL_PHI, TAIL_RESID, TAIL_RESTRICT)
 from .errors import ConfigError, DimensionError
 from .grid import SpatialGrid, TemporalGrid, Trajectory
-from .stepper import RungeKuttaStepper
+from .stepper import ComposedStepper, RungeKuttaStepper, _LFStepper
 
 CYCLE_KINDS = ("v", "f")
 RELAXATION_KINDS = ("f", "fcf")
@@ -136,14 +136,26 @@ class MgritLevel:
         return self._h._g[self.index].view(self.n_intervals + 1, 1, -1)
 
 
-def _check_stepper(s, l: int, nx: int) -> RungeKuttaStepper:
-    if not isinstance(s, RungeKuttaStepper):
+_PROPAGATORS = (RungeKuttaStepper, _LFStepper, ComposedStepper)
+
+
+def _check_stepper(s, l: int, nx: int):
+    if not isinstance(s, _PROPAGATORS):
         raise ConfigError(
-            f"level {l}: the B200 hierarchy runs paper_2104_09404_b200."
-            f"RungeKuttaStepper propagators, got {type(s).__name__}")
+            f"level {l}: the B200 hierarchy runs this package's propagators "
+            f"(RungeKuttaStepper, MatchedLF*, RediscretizedLF, ComposedStepper), "
+            f"got {type(s).__name__}")
     if s.nx != nx:
         raise DimensionError(f"level {l}: stepper mesh has {s.nx} cells, state has {nx}")
     return s
+
+
+def _nx_limit(s) -> int:
+    inner = s.inner if isinstance(s, ComposedStepper) else s
+    if isinstance(inner, RungeKuttaStepper):
+        op = inner.operator
+        return dev._lib.max_nx(op.config.weno.degree, op.model.abi_model)
+    return 2048   # one-step LF family (kMaxLfNx)
 
 
 class MgritHierarchy:
@@ -167,12 +179,11 @@ class MgritHierarchy:
         self.nx = nx = u0.shape[1]
         self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
         if not dev.emulated():
-            for s in self.steppers:
-                op = s.operator
-                lim = dev._lib.max_nx(op.config.weno.degree, op.model.abi_model)
+            for l, s in enumerate(self.steppers):
+                lim = _nx_limit(s)
                 if nx > lim:
-                    raise ConfigError(f"N_x = {nx} exceeds the field limit {lim} of this "
-                                      f"build for WENO{op.config.weno.order}")
+                    raise ConfigError(f"level {l}: N_x = {nx} exceeds the field limit "
+                                      f"{lim} of this build for {type(s).__name__}")
         self._u0 = u0[0].contiguous()
         self.n = [time_grid.n_steps // m ** l for l in range(L)]
         self.levels = [MgritLevel(self, l, time_grid.dt * m ** l, self.n[l], steppers[l])

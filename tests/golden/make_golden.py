@@ -24,6 +24,7 @@ GPU box has no /root/reference: the tests read only these committed files.
 """
 from __future__ import annotations
 
+import dataclasses
 import json
 import os
 import sys
@@ -313,6 +314,134 @@ def mgrit_cases():
         json.dump(meta, f, indent=1)
 
 
+# ---------------------------------------------------------------------------
+# one-step Lax-Friedrichs family (stepper.py:85-188) -- SURVEY.md 8(f) rank 1
+# ---------------------------------------------------------------------------
+
+def oracle_for(st, dx):
+    """Oracle stepper equivalent to a reference stepper object."""
+    if isinstance(st, R.ComposedStepper):
+        inner = oracle_for(st.inner, dx)
+        inner.repeats *= st.repeats
+        inner.dt = st.dt
+        return inner
+    if isinstance(st, (R.MatchedLFFine, R.RediscretizedLF)):
+        return oracle.OracleStepper(k=0, rk_order=1, dt=st.dt, dx=dx, scheme=1, nthreads=1)
+    if isinstance(st, R.MatchedLFCoarse):
+        fdt = st.dt if st.order == 0 else st.dt_fine
+        return oracle.OracleStepper(k=0, rk_order=1, dt=st.dt, dx=dx, scheme=2,
+                                    lf_order=st.order, m_eff=st.m_effective,
+                                    formula_dt=fdt, nthreads=1)
+    op = st.rhs.__self__
+    return oracle.OracleStepper(model=op.model.kind, k=op.config.weno.degree,
+                                rk_order=st.order, dt=st.dt, dx=dx,
+                                eps=op.config.weno.epsilon, nthreads=1)
+
+
+def lf_vectors():
+    rng = np.random.default_rng(7)
+    out, index = {}, []
+    sg = R.SpatialGrid(1.0, 48)
+    model = R.make_model("burgers")
+    dt = 0.2 * sg.dx
+    op = R.SemiDiscreteOperator(model, sg, R.FluxConfig("lf", R.WenoConfig(5)))
+    cases = [("fine", R.MatchedLFFine(model, sg, dt)),
+             ("redisc", R.RediscretizedLF(model, sg, 4 * dt))]
+    for m_eff in (1, 2, 4, 16):
+        for order in (0, 1):
+            cases.append((f"matched{order}_m{m_eff}",
+                          R.MatchedLFCoarse(model, sg, dt, m_eff, order)))
+    cases.append(("composed_fine3", R.ComposedStepper(R.MatchedLFFine(model, sg, dt), 3)))
+    cases.append(("composed_rk3x4", R.ComposedStepper(R.RungeKuttaStepper(op.rhs, dt, 3), 4)))
+    n = 0
+    for name, st in cases:
+        for shape in ((3, 1, 48), (1, 48)):
+            u = make_fields(rng, shape, "shock")
+            with np.errstate(all="ignore"):
+                y = st.advance(u)
+            mine = oracle_for(st, sg.dx).advance(u)
+            assert np.array_equal(mine, y, equal_nan=True), name
+            key = f"lf{n:03d}"
+            out[key + "_in"], out[key + "_out"] = u, y
+            meta = dict(key=key, name=name, shape=list(shape), dx=sg.dx, dt_fine=dt)
+            if isinstance(st, R.MatchedLFCoarse):
+                meta.update(kind="matched", order=st.order, m_eff=st.m_effective)
+            elif isinstance(st, R.ComposedStepper):
+                meta.update(kind="composed", repeats=st.repeats,
+                            inner="rk3" if isinstance(st.inner, R.RungeKuttaStepper) else "fine")
+            else:
+                meta.update(kind="onestep", dt=st.dt)
+            index.append(meta)
+            n += 1
+    np.savez_compressed(os.path.join(HERE, "lf_vectors.npz"), **out)
+    with open(os.path.join(HERE, "lf_vectors.json"), "w") as f:
+        json.dump(index, f, indent=0)
+    print(f"lf vectors: {len(index)}")
+
+
+LF_CONFIGS = [("fine_match_stationary_vcycle.cfg", None),
+              ("fine_match_moving_fcycle.cfg", None),
+              ("restriction_guess_fcf_relax.cfg", None),
+              ("restriction_guess_f_relax.cfg", None),
+              ("two_level_exact.cfg", None),
+              ("cfl_matched_fe.cfg", None),
+              ("fine_match_refinement_vcycle.cfg", 2)]
+
+
+def lf_mgrit_cases():
+    arrays, meta = {}, []
+    cfg_dir = "/root/reference/pkg/configs"
+    for fname, limit in LF_CONFIGS:
+        base = R.load_config(os.path.join(cfg_dir, fname))
+        cols = [(None, base)] if base.sweep is None else [
+            (raw, R.apply_sweep_value(dataclasses.replace(base, sweep=None, sweep_values=()),
+                                      base.sweep, raw))
+            for raw in base.sweep_values]
+        if limit:
+            cols = cols[:limit]
+        for raw, col in cols:
+            res = R.run_experiment(col)
+            sg = R.SpatialGrid(col.length, col.n_x)
+            tg = R.TemporalGrid(col.horizon, col.n_t)
+            u0 = R.initial_state(col.ic, sg, col.length)
+            # oracle cross-check with the reference's own steppers mapped
+            from mgritlab.harness import build_steppers as ref_build_steppers
+            steppers = ref_build_steppers(col, R.make_model(col.problem), sg, tg)
+            ost = [oracle_for(st, sg.dx) for st in steppers]
+            oref = mgrit_oracle.march(ost[0], u0, col.n_t)
+            o_opts = mgrit_oracle.Options(n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                                          relaxation=col.relaxation,
+                                          guess=col.restriction_guess,
+                                          max_iters=col.max_iters)
+            _, orec = mgrit_oracle.mgrit_solve(ost, u0, col.n_t, tg.dt, o_opts, reference=oref)
+            assert orec.diverged_at == res.record.diverged_at, fname
+            ok = np.isfinite(res.record.errors)
+            assert np.allclose(orec.errors[ok], res.record.errors[ok], rtol=1e-12), fname
+            name = fname[:-4] + ("" if raw is None else "__" + str(raw).replace(" ", ""))
+            arrays[name + "__u0"] = u0
+            arrays[name + "__errors"] = res.record.errors
+            arrays[name + "__residuals"] = res.record.residuals
+            meta.append(dict(name=name, model="burgers", n_x=col.n_x, n_t=col.n_t,
+                             horizon=col.horizon, dt=tg.dt, length=col.length,
+                             stepper=list(col.stepper), weno_order=list(col.weno_order),
+                             coarse=col.coarse, n_levels=col.n_levels, m=col.m,
+                             cycle=col.cycle, relaxation=col.relaxation,
+                             guess=col.restriction_guess, max_iters=col.max_iters,
+                             semantics="harness", diverged_at=res.record.diverged_at,
+                             has_traj=False))
+            print(f"{name}: diverged_at={res.record.diverged_at} err[:3]={res.record.errors[:3]}")
+    np.savez_compressed(os.path.join(HERE, "lf_mgrit_cases.npz"), **arrays)
+    with open(os.path.join(HERE, "lf_mgrit_cases.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 if __name__ == "__main__":
-    phi_vectors()
-    mgrit_cases()
+    import sys as _sys
+    which = _sys.argv[1:] or ["phi", "mgrit", "lf"]
+    if "phi" in which:
+        phi_vectors()
+    if "mgrit" in which:
+        mgrit_cases()
+    if "lf" in which:
+        lf_vectors()
+        lf_mgrit_cases()

@@ -21,7 +21,8 @@ def _rows(t, stride, n, nx, off=0):
 def _params(phi, regime):
     return oracle.make_params(model=_MODEL[phi.model], k=phi.weno_k, rk_order=phi.rk_order,
                               dt=phi.dt, dx=phi.dx, eps=phi.epsilon, speed=phi.speed,
-                              regime=regime)
+                              regime=regime, scheme=phi.scheme, lf_order=phi.lf_order,
+                              m_eff=phi.m_eff, repeats=phi.repeats)
 
 
 def _add_g(y, mode, g):

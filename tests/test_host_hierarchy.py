@@ -78,3 +78,29 @@ def test_solve_matches_oracle(cycle, relax, guess):
     assert np.array_equal(traj.values, otraj)
     np.testing.assert_allclose(rec.residuals, orec.residuals, rtol=1e-12)
     np.testing.assert_allclose(rec.errors, orec.errors, rtol=1e-12)
+
+
+def test_lf_family_hierarchy_matches_oracle():
+    """matched-lf fine + matched-1 coarse and the exact composition through
+    the hierarchy bookkeeping (emulated kernels) vs the oracle."""
+    import json, os
+    meta = {m["name"]: m for m in json.load(open(os.path.join(
+        os.path.dirname(__file__), "golden", "lf_mgrit_cases.json")))}
+    data = np.load(os.path.join(os.path.dirname(__file__), "golden", "lf_mgrit_cases.npz"))
+    for name in ("two_level_exact", "restriction_guess_fcf_relax__injection"):
+        spec = meta[name]
+        u0 = data[name + "__u0"]
+        sg = P.SpatialGrid(spec["length"], spec["n_x"])
+        tg = P.TemporalGrid(spec["horizon"], spec["n_t"])
+        steppers = P.build_steppers(P.make_model("burgers"), sg, tg, n_levels=spec["n_levels"],
+                                    m=spec["m"], stepper=spec["stepper"], coarse=spec["coarse"])
+        ref = P.serial.march(steppers[0], u0, spec["n_t"])
+        opts = P.MgritOptions(n_levels=spec["n_levels"], m=spec["m"], cycle=spec["cycle"],
+                              relaxation=spec["relaxation"], guess=spec["guess"],
+                              max_iters=spec["max_iters"])
+        _, rec = P.mgrit_solve(steppers, u0, tg, sg, opts, reference=ref,
+                               return_trajectory=False)
+        want = data[name + "__errors"]
+        ok = np.isfinite(want)
+        np.testing.assert_allclose(rec.errors[ok], want[ok], rtol=1e-10)
+        assert rec.diverged_at == spec["diverged_at"]
