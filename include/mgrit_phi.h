@@ -59,6 +59,8 @@ extern "C" {
 #define MGP_SCHEME_RK_WENO 0     /* RungeKuttaStepper over WENO + global LF (stepper.py:68-82) */
 #define MGP_SCHEME_LF_ONESTEP 1  /* MatchedLFFine / RediscretizedLF (stepper.py:102-114,155-167) */
 #define MGP_SCHEME_LF_MATCHED 2  /* MatchedLFCoarse order 0/1 (stepper.py:117-152) */
+#define MGP_SCHEME_RK_WENO_ROE 3 /* as 0 with the Roe flux + entropy fix, Burgers
+                                    (flux.py:91-126), nx <= 4096 */
 
 /* how "+ g" is applied after a propagator application */
 #define MGP_G_NONE 0   /* no addition (advance, serial march)              */

@@ -197,6 +197,27 @@ static void rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
         for (int s = 0; s <= 2 * k; ++s) w[s] = c[1 + k - s];
         wk->ur[i] = recon(t, p->regime, w);
     }
+    if (p->scheme == 3) {
+        /* Roe flux with Harten-Hyman entropy fix, Burgers (flux.py:91-126,
+         * models.py:125-128): strength = 1*jump, speed from entropy_fix,
+         * F = 0.5 (fL + fR) - 0.5 (speed * jump). */
+        for (int64_t i = 0; i < nx; ++i) {
+            const double l = wk->ul[i], r = wk->ur[i];
+            const double fl = (0.5 * l) * l, fr = (0.5 * r) * r;
+            const double lam = 0.5 * (l + r);
+            const double a = lam - l, b = r - lam;
+            const double inner = (a >= b || isnan(a)) ? a : b;      /* np.maximum */
+            const double delta = (0.0 >= inner) ? 0.0 : inner;      /* NaN -> inner */
+            const double alam = fabs(lam);
+            const double speed = (alam < delta) ? 0.5 * ((lam * lam) / delta + delta) : alam;
+            wk->F[i] = (0.5 * (fl + fr)) - (0.5 * (speed * (r - l)));
+        }
+        for (int64_t i = 0; i < nx; ++i) {
+            const double fm = wk->F[i == 0 ? nx - 1 : i - 1];
+            A[i] = (-(wk->F[i] - fm)) / p->dx;
+        }
+        return;
+    }
     double alpha;
     if (p->model == ORA_MODEL_BURGERS) {
         /* np.max over interfaces (NaN-propagating), then np.maximum */
@@ -296,7 +317,7 @@ static void phi_once(const ora_params *p, const ora_tables *t, ora_work *wk,
                      const double *u, double *out) {
     const int64_t nx = wk->nx;
     double *A = wk->A, *u1 = wk->u1, *u2 = wk->u2;
-    if (p->scheme != 0) {
+    if (p->scheme == 1 || p->scheme == 2) {
         lf_field(p, wk, u, out);
         return;
     }
@@ -332,7 +353,8 @@ static int check_params(const ora_params *p, int64_t nx) {
     if (p->scheme == 1 || p->scheme == 2)
         return (p->model != ORA_MODEL_BURGERS || nx < 1 ||
                 (p->scheme == 2 && (p->m_eff < 1 || p->lf_order < 0 || p->lf_order > 1)));
-    if (p->scheme != 0) return 1;
+    if (p->scheme != 0 && p->scheme != 3) return 1;
+    if (p->scheme == 3 && p->model != ORA_MODEL_BURGERS) return 1;
     if (p->k < 0 || p->k > 3) return 1;
     if (p->rk_order < 0 || p->rk_order > 3) return 1;
     if (p->model != ORA_MODEL_BURGERS && p->model != ORA_MODEL_ADVECTION) return 1;

@@ -25,7 +25,7 @@ MGP_OK, MGP_EINVAL, MGP_ECUDA = 0, 1, 2
 SUM_SEQ, SUM_LANE2 = 0, 1
 G_NONE, G_ZERO, G_ARRAY = 0, 1, 2
 TAIL_NONE, TAIL_PHI, TAIL_RESTRICT, TAIL_RESID = 0, 1, 2, 3
-SCHEME_RK_WENO, SCHEME_LF_ONESTEP, SCHEME_LF_MATCHED = 0, 1, 2
+SCHEME_RK_WENO, SCHEME_LF_ONESTEP, SCHEME_LF_MATCHED, SCHEME_RK_WENO_ROE = 0, 1, 2, 3
 GUESS_LAST_STEP, GUESS_INJECTION = 0, 1
 
 NVCC_FLAGS = [

@@ -125,6 +125,10 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
 
 constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
 
+// kernel-internal model id: Burgers with the Roe flux (mgp_phi.scheme ==
+// MGP_SCHEME_RK_WENO_ROE), no global alpha, NaN kept local like the reference
+constexpr int kModelBurgersRoe = 2;
+
 #ifndef MGP_SLIDE_UNROLL
 #define MGP_SLIDE_UNROLL 1
 #endif
@@ -352,7 +356,7 @@ struct Field {
     // bits of this thread's NaN-propagating max |u| (Burgers).
     __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
         unsigned long long m = 0;
-        constexpr bool kCheck = (MODEL == MGP_MODEL_ADVECTION);
+        constexpr bool kCheck = (MODEL != MGP_MODEL_BURGERS);
         if (P == 0 && K > 0) {
             const int tid = threadIdx.x;
             const int side = (tid >> 5) & 1;              // warp-uniform
@@ -495,6 +499,23 @@ struct Field {
     __device__ __forceinline__ double lf(const Consts &k, double ul, double ur,
                                          double half_alpha) const {
         double fl, fr;
+        if (MODEL == kModelBurgersRoe) {
+            // Roe flux with Harten-Hyman entropy fix for Burgers
+            // (flux.py:91-126, models.py:125-128): lam = 0.5 (uL + uR),
+            // delta = max(0, max(lam - uL, uR - lam)) (np.maximum, NaN-
+            // propagating), speed = |lam| < delta ? 0.5 (lam lam / delta + delta)
+            // : |lam|; F = 0.5 (f(uL) + f(uR)) - 0.5 (speed (uR - uL))
+            fl = (0.5 * ul) * ul;
+            fr = (0.5 * ur) * ur;
+            const double lam = 0.5 * (ul + ur);
+            const double a = lam - ul, b = ur - lam;
+            const double inner = (a >= b || a != a) ? a : b;
+            const double delta = (0.0 >= inner || 0.0 != 0.0) ? 0.0 : inner;
+            const double alam = fabs(lam);
+            const double speed = (alam < delta) ? 0.5 * ((lam * lam) / delta + delta) : alam;
+            const double diss = speed * (ur - ul);
+            return (0.5 * (fl + fr)) - (0.5 * diss);
+        }
         if (MODEL == MGP_MODEL_BURGERS) {
             fl = (0.5 * ul) * ul;
             fr = (0.5 * ur) * ur;
@@ -1033,7 +1054,8 @@ int env_int(const char *name) {
 // sequential coarse solve are split for latency (MGP_MARCH_CS overrides).
 int cluster_size(const mgp_sweep_args &a) {
     const int64_t nx = a.phi.nx;
-    const bool cl_ok = a.phi.weno_k == 2 && a.phi.model == MGP_MODEL_BURGERS;
+    const bool cl_ok = a.phi.weno_k == 2 && a.phi.model == MGP_MODEL_BURGERS &&
+                       a.phi.scheme == MGP_SCHEME_RK_WENO;
     if (nx > kMaxNx) {
         int cs = 2;
         while (nx / cs > kMaxNx || nx % cs) cs *= 2;
@@ -1153,7 +1175,10 @@ int validate(const mgp_sweep_args *a) {
     if (!a) return MGP_EINVAL;
     const mgp_phi &p = a->phi;
     if (p.repeats < 1) return MGP_EINVAL;
-    if (p.scheme != MGP_SCHEME_RK_WENO) {
+    if (p.scheme == MGP_SCHEME_RK_WENO_ROE &&
+        (p.model != MGP_MODEL_BURGERS || p.nx > kMaxNx))
+        return MGP_EINVAL;
+    if (p.scheme != MGP_SCHEME_RK_WENO && p.scheme != MGP_SCHEME_RK_WENO_ROE) {
         if (p.scheme != MGP_SCHEME_LF_ONESTEP && p.scheme != MGP_SCHEME_LF_MATCHED)
             return MGP_EINVAL;
         if (p.model != MGP_MODEL_BURGERS) return MGP_EINVAL;   // stepper.py:95-99
@@ -1215,6 +1240,7 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (rc != MGP_OK) return rc;
     if (args->n_chunks == 0) return MGP_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (args->phi.scheme == MGP_SCHEME_RK_WENO_ROE) return launch_m<kModelBurgersRoe>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
     if (args->phi.model == MGP_MODEL_BURGERS) return launch_m<MGP_MODEL_BURGERS>(*args, st);

@@ -4,8 +4,9 @@ Mirrors reference ``pkg/src/mgritlab/flux.py``: ``WenoConfig`` /
 ``FluxConfig`` validation (flux.py:35-67), ``SemiDiscreteOperator``
 constructor checks (:129-145) and ``rhs`` (:159-161).  The operator only
 holds parameters; ``rhs(field)`` runs on the GPU (``mgp_sweep`` with
-rk_order 0).  The Roe flux (flux.py:91-126) is outside the GPU path's scope
-and is rejected with ConfigError, as are systems; there is no CPU fallback.
+rk_order 0).  The Roe flux with the Harten-Hyman entropy fix
+(flux.py:91-126) is supported for Burgers; systems are rejected with
+ConfigError; there is no CPU fallback.
 """
 from __future__ import annotations
 
@@ -14,7 +15,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import device as dev
-from ._lib import MgpPhi, SCHEME_RK_WENO, TAIL_PHI
+from ._lib import MgpPhi, SCHEME_RK_WENO, SCHEME_RK_WENO_ROE, TAIL_PHI
 from .errors import ConfigError, DimensionError
 from .grid import SpatialGrid
 from .models import ConservationModel
@@ -66,9 +67,9 @@ class SemiDiscreteOperator:
         if space_grid.n_cells < 2 * config.weno.degree + 1:
             raise ConfigError(f"{space_grid.n_cells} cells cannot support order "
                               f"{config.weno.order} reconstruction")
-        if config.kind != "lf":
-            raise ConfigError("the B200 path implements the Lax-Friedrichs flux; "
-                              "the Roe flux is out of scope")
+        if config.kind == "roe" and getattr(model, "kind", "") != "burgers":
+            raise ConfigError("the B200 path implements the Roe flux for Burgers only "
+                              "(systems are out of scope)")
         if getattr(model, "n_components", None) != 1 or not hasattr(model, "abi_model"):
             raise ConfigError(f"model '{getattr(model, 'kind', model)}' is not a "
                               "scalar model of the B200 path")
@@ -82,7 +83,8 @@ class SemiDiscreteOperator:
                       int(rk_order), int(regime), int(self.space_grid.n_cells),
                       float(dt), float(self.space_grid.dx),
                       float(self.config.weno.epsilon), float(self.model.speed),
-                      SCHEME_RK_WENO, 0, 0, 1)
+                      SCHEME_RK_WENO_ROE if self.config.kind == "roe" else SCHEME_RK_WENO,
+                      0, 0, 1)
 
     def rhs(self, field_):
         """SemiDiscreteOperator.rhs (flux.py:159-161) on the GPU.  Returns the

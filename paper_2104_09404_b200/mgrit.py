@@ -154,6 +154,8 @@ def _nx_limit(s) -> int:
     inner = s.inner if isinstance(s, ComposedStepper) else s
     if isinstance(inner, RungeKuttaStepper):
         op = inner.operator
+        if op.config.kind == "roe":
+            return 4096
         return dev._lib.max_nx(op.config.weno.degree, op.model.abi_model)
     return 2048   # one-step LF family (kMaxLfNx)
 

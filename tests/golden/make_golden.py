@@ -335,7 +335,8 @@ def oracle_for(st, dx):
     op = st.rhs.__self__
     return oracle.OracleStepper(model=op.model.kind, k=op.config.weno.degree,
                                 rk_order=st.order, dt=st.dt, dx=dx,
-                                eps=op.config.weno.epsilon, nthreads=1)
+                                eps=op.config.weno.epsilon, nthreads=1,
+                                scheme=3 if op.config.kind == "roe" else 0)
 
 
 def lf_vectors():
@@ -352,6 +353,10 @@ def lf_vectors():
             cases.append((f"matched{order}_m{m_eff}",
                           R.MatchedLFCoarse(model, sg, dt, m_eff, order)))
     cases.append(("composed_fine3", R.ComposedStepper(R.MatchedLFFine(model, sg, dt), 3)))
+    for k in (0, 1, 2, 3):
+        for rk in (1, 2, 3):
+            rop = R.SemiDiscreteOperator(model, sg, R.FluxConfig("roe", R.WenoConfig(2 * k + 1)))
+            cases.append((f"roe_k{k}_rk{rk}", R.RungeKuttaStepper(rop.rhs, dt, rk)))
     cases.append(("composed_rk3x4", R.ComposedStepper(R.RungeKuttaStepper(op.rhs, dt, 3), 4)))
     n = 0
     for name, st in cases:
@@ -364,7 +369,10 @@ def lf_vectors():
             key = f"lf{n:03d}"
             out[key + "_in"], out[key + "_out"] = u, y
             meta = dict(key=key, name=name, shape=list(shape), dx=sg.dx, dt_fine=dt)
-            if isinstance(st, R.MatchedLFCoarse):
+            if isinstance(st, R.RungeKuttaStepper):
+                rop = st.rhs.__self__
+                meta.update(kind="roe", k=rop.config.weno.degree, rk=st.order, dt=st.dt)
+            elif isinstance(st, R.MatchedLFCoarse):
                 meta.update(kind="matched", order=st.order, m_eff=st.m_effective)
             elif isinstance(st, R.ComposedStepper):
                 meta.update(kind="composed", repeats=st.repeats,
@@ -385,7 +393,13 @@ LF_CONFIGS = [("fine_match_stationary_vcycle.cfg", None),
               ("restriction_guess_f_relax.cfg", None),
               ("two_level_exact.cfg", None),
               ("cfl_matched_fe.cfg", None),
-              ("fine_match_refinement_vcycle.cfg", 2)]
+              ("fine_match_refinement_vcycle.cfg", 2),
+              # Roe flux with entropy fix (flux.py:91-126), SURVEY 8(f) rank 2
+              ("high_order_burgers_roe.cfg", None),
+              ("order_mix_space_roe.cfg", None),
+              ("order_mix_space_time_up_roe.cfg", None),
+              ("cfl_weno5_fe_roe.cfg", None),
+              ("cfl_weno1_ssprk3_roe.cfg", 3)]
 
 
 def lf_mgrit_cases():
@@ -421,7 +435,7 @@ def lf_mgrit_cases():
             arrays[name + "__u0"] = u0
             arrays[name + "__errors"] = res.record.errors
             arrays[name + "__residuals"] = res.record.residuals
-            meta.append(dict(name=name, model="burgers", n_x=col.n_x, n_t=col.n_t,
+            meta.append(dict(name=name, model="burgers", n_x=col.n_x, n_t=col.n_t, flux=col.flux,
                              horizon=col.horizon, dt=tg.dt, length=col.length,
                              stepper=list(col.stepper), weno_order=list(col.weno_order),
                              coarse=col.coarse, n_levels=col.n_levels, m=col.m,

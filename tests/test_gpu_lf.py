@@ -1,8 +1,8 @@
 """GPU parity of the one-step Lax-Friedrichs family (matched fine / coarse
-order 0 and 1, rediscretised) and of ComposedStepper against the reference's
-own outputs -- propagator vectors and the checked-in study configs
-(pkg/configs/fine_match_*, restriction_guess_*, cfl_matched_fe,
-two_level_exact, fine_match_refinement_vcycle)."""
+order 0 and 1, rediscretised), of ComposedStepper and of the Roe flux with
+entropy fix against the reference's own outputs -- propagator vectors and
+the checked-in study configs (pkg/configs/fine_match_*, restriction_guess_*,
+cfl_matched_fe, two_level_exact, fine_match_refinement_vcycle, *_roe)."""
 import json
 import os
 
@@ -17,6 +17,9 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 def _stepper(c, sg):
     model = P.make_model("burgers")
+    if c["kind"] == "roe":
+        op = P.SemiDiscreteOperator(model, sg, P.FluxConfig("roe", P.WenoConfig(2 * c["k"] + 1)))
+        return P.RungeKuttaStepper(op.rhs, c["dt"], c["rk"])
     if c["kind"] == "onestep":
         return P.MatchedLFFine(model, sg, c["dt"])
     if c["kind"] == "matched":
@@ -48,7 +51,8 @@ def test_lf_study_configs_match_reference():
         assert tg.dt == spec["dt"]
         steppers = P.build_steppers(P.make_model("burgers"), sg, tg, n_levels=spec["n_levels"],
                                     m=spec["m"], weno_order=spec["weno_order"],
-                                    stepper=spec["stepper"], coarse=spec["coarse"])
+                                    stepper=spec["stepper"], coarse=spec["coarse"],
+                                    flux=spec.get("flux", "lf"))
         serial = P.solve_serial(steppers[0], u0, tg, sg, P.make_model("burgers"))
         opts = P.MgritOptions(n_levels=spec["n_levels"], m=spec["m"], cycle=spec["cycle"],
                               relaxation=spec["relaxation"], guess=spec["guess"],

@@ -17,9 +17,13 @@ def test_config_errors_mirror_reference():
     sg = P.SpatialGrid(1.0, 4)
     with pytest.raises(P.ConfigError):   # 4 cells cannot support WENO5 (flux.py:138-141)
         P.SemiDiscreteOperator(P.make_model("burgers"), sg, P.FluxConfig("lf", P.WenoConfig(5)))
-    with pytest.raises(P.ConfigError):   # Roe is out of the GPU path's scope
-        P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, 8),
+    with pytest.raises(P.ConfigError):   # Roe: Burgers only (systems out of scope)
+        P.SemiDiscreteOperator(P.make_model("advection"), P.SpatialGrid(1.0, 8),
                                P.FluxConfig("roe", P.WenoConfig(1)))
+    with pytest.raises(P.ConfigError):   # matched operators: scalar Burgers only
+        P.MatchedLFFine(P.make_model("advection"), P.SpatialGrid(1.0, 8), 0.1)
+    with pytest.raises(P.ConfigError):
+        P.MatchedLFCoarse(P.make_model("burgers"), P.SpatialGrid(1.0, 8), 0.1, 2, 2)
     with pytest.raises(P.ConfigError):
         P.make_model("euler")
     op = P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, 8),
