@@ -453,6 +453,96 @@ class MgritHierarchy:
         self._fsrc = self._cur
         self._pristine = False
 
+    def relax_to_host(self, c_points_host: torch.Tensor, traj_host: torch.Tensor,
+                      pieces: int = 2, graph: bool = False) -> None:
+        """One relaxation of the finest level (``relax(0)``) fed from and
+        written back to pinned host memory, pipelined over pieces of
+        CF-intervals: the C-points of piece k+1 travel host->device and the
+        trajectory rows of piece k-1 device->host while piece k is relaxed
+        (PCIe is full duplex; the copies run on their own streams).  Input:
+        the C-points (N_t/m + 1 rows); output: the relaxed finest trajectory
+        (N_t + 1 rows), i.e. ``fine_values()`` after ``relax(0)``; the
+        hierarchy holds the relaxed iterate afterwards.  Asynchronous on the
+        current stream (synchronise before reading the host output).
+        ``graph=True`` captures the step into a CUDA graph on first use (one
+        per buffer parity) and replays it.  Measured on B200 for config 2:
+        2 pieces best (more pieces under-fill the GPU per launch; reading /
+        writing pinned memory directly from the kernels was slower)."""
+        if graph:
+            return self._relax_to_host_graph(c_points_host, traj_host, pieces)
+        return self._relax_to_host(c_points_host, traj_host, pieces, capturing=False)
+
+    def _relax_to_host_graph(self, c_points_host, traj_host, pieces):
+        key = (c_points_host.data_ptr(), traj_host.data_ptr(), pieces, self._cur,
+               self.options.relaxation)
+        cache = self.__dict__.setdefault("_graphs", {})
+        if key not in cache:
+            cur = self._cur
+            self._relax_to_host(c_points_host, traj_host, pieces, capturing=False)  # warm-up
+            torch.cuda.synchronize()
+            self._cur = self._fsrc = cur
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._relax_to_host(c_points_host, traj_host, pieces, capturing=True)
+            cache[key] = (g, self._cur)
+            self._cur = self._fsrc = cur
+        g, after = cache[key]
+        g.replay()
+        self._cur = self._fsrc = after
+        self._pristine = False
+
+    def _relax_to_host(self, c_points_host, traj_host, pieces, capturing):
+        m, nx, nt = self.options.m, self.nx, self.n[0]
+        nc = self.n_chunks0
+        regime = dev.regime_for_batch(nc)
+        phi = self._phi(0, regime)
+        fcf = self.options.relaxation == "fcf"
+        comp = torch.cuda.current_stream()
+        if not hasattr(self, "_io"):
+            self._io = (torch.cuda.Stream(), torch.cuda.Stream(),
+                        torch.empty(nt + 1, nx, dtype=dev.DTYPE, device=self.device))
+        h2d, d2h, traj = self._io
+        src = self._cur
+        cs = self._c[src]
+        dst = self._other(src) if fcf else src
+        cd = self._c[dst]
+        ch = c_points_host.reshape(nc + 1, nx)
+        th = traj_host.reshape(nt + 1, nx)
+        if not capturing:
+            comp.wait_stream(d2h)   # the previous call's copies are done with traj
+        h2d.wait_stream(comp)       # ... and its kernels with the C-point buffers
+        bounds = [nc * k // pieces for k in range(pieces + 1)]
+        for k in range(pieces):
+            a, b = bounds[k], bounds[k + 1]
+            if a == b:
+                continue
+            last = b == nc
+            with torch.cuda.stream(h2d):
+                cs[a:b + (1 if last else 0)].copy_(ch[a:b + (1 if last else 0)],
+                                                   non_blocking=True)
+            comp.wait_stream(h2d)
+            if fcf:
+                if a == 0:
+                    cd[0].copy_(cs[0])
+                # fused F + C relaxation of chunks [a, b): new C-points a+1..b
+                dev.sweep(phi, n_chunks=b - a, start=cs[a], start_stride=nx,
+                          n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI, tail_regime=regime,
+                          tail_g_mode=G_ZERO, tail_out=cd[a + 1], to_s=nx,
+                          what="relax_to_host/fc")
+            # final F-relaxation with every node stored
+            traj[a * m: b * m + 1: m].copy_(cd[a:b + 1])
+            dev.sweep(phi, n_chunks=b - a, start=cd[a], start_stride=nx, n_steps=m - 1,
+                      g_mode=G_ZERO, store=traj[a * m + 1], st_cs=m * nx, st_ss=nx,
+                      what="relax_to_host/f")
+            d2h.wait_stream(comp)
+            with torch.cuda.stream(d2h):
+                rows = slice(a * m, b * m + (1 if last else 0))
+                th[rows].copy_(traj[rows], non_blocking=True)
+        comp.wait_stream(d2h)
+        self._cur = dst
+        self._fsrc = dst
+        self._pristine = False
+
     def c_points(self) -> torch.Tensor:
         """Current finest-level C-points (N_t/m + 1, 1, N), device view."""
         return self._c[self._cur].view(-1, 1, self.nx)

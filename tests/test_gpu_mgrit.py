@@ -190,3 +190,42 @@ def test_large_mesh_mgrit_on_clusters():
     assert np.array_equal(traj.values, otraj)
     np.testing.assert_allclose(rec.residuals, orec.residuals, rtol=1e-10)
     np.testing.assert_allclose(rec.errors, orec.errors, rtol=1e-10)
+
+
+@pytest.mark.parametrize("relaxation,pieces", [("fcf", 8), ("fcf", 1), ("f", 3), ("fcf", 1000)])
+def test_relax_to_host_equals_relax_then_fine_values(relaxation, pieces):
+    pb = P.Problem(name="io", n_x=64, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4,
+                   relaxation=relaxation)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    serial = P.serial.march(steppers[0], u0, pb.n_t)
+    c_host = serial[::4, 0].cpu().pin_memory()
+    out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
+    h = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    h.relax_to_host(c_host, out, pieces=pieces)
+    torch.cuda.synchronize()
+    g = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    g.load_c_points(c_host)
+    g.relax(0)
+    assert torch.equal(out, g.fine_values().cpu())
+    # the hierarchy state afterwards is the relaxed one
+    assert torch.equal(h.fine_values().cpu(), out)
+
+
+def test_relax_to_host_graph_replay():
+    pb = P.Problem(name="io", n_x=64, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    serial = P.serial.march(steppers[0], u0, pb.n_t)
+    c_host = serial[::4, 0].cpu().pin_memory()
+    out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
+    h = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    g = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    for _ in range(3):          # both buffer parities, captured then replayed
+        h.relax_to_host(c_host, out, pieces=4, graph=True)
+        torch.cuda.synchronize()
+        g.load_c_points(c_host)
+        g.relax(0)
+        assert torch.equal(out, g.fine_values().cpu())
