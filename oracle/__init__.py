@@ -29,6 +29,14 @@ _LIB_PATH = os.path.join(_HERE, "libphi_oracle.so")
 
 MODEL_BURGERS = 0
 MODEL_ADVECTION = 1
+MODEL_SHALLOW_WATER = 2
+_MODELS = {"burgers": MODEL_BURGERS, "advection": MODEL_ADVECTION,
+           "shallow-water": MODEL_SHALLOW_WATER}
+
+
+class PhysicalStateOracleError(ValueError):
+    """The oracle met a non-positive depth (the reference raises
+    PhysicalStateError there, models.py:147-153)."""
 SUM_SEQ = 0
 SUM_LANE2 = 1
 
@@ -39,7 +47,8 @@ class OraParams(ctypes.Structure):
                 ("dt", ctypes.c_double), ("dx", ctypes.c_double),
                 ("eps", ctypes.c_double), ("speed", ctypes.c_double),
                 ("scheme", ctypes.c_int32), ("lf_order", ctypes.c_int32),
-                ("m_eff", ctypes.c_int32), ("repeats", ctypes.c_int32)]
+                ("m_eff", ctypes.c_int32), ("repeats", ctypes.c_int32),
+                ("gravity", ctypes.c_double)]
 
 
 _lib = None
@@ -81,38 +90,41 @@ def _ptr(a):
 
 def make_params(*, model="burgers", k=2, rk_order=3, dt=1e-3, dx=1.0 / 64,
                 eps=1e-6, speed=1.0, regime=SUM_SEQ, scheme=0, lf_order=0, m_eff=1,
-                repeats=1) -> OraParams:
+                repeats=1, gravity=9.81) -> OraParams:
     """scheme 0: RK over WENO/LF; 1: one-step LF (matched-lf-fine,
     rediscretized-lf), 2: matched coarse LF of order lf_order emulating m_eff
     fine steps (dt = the step the formula multiplies, see include/mgrit_phi.h);
     repeats: ComposedStepper count."""
-    m = MODEL_BURGERS if model == "burgers" else MODEL_ADVECTION
-    return OraParams(m, int(k), int(rk_order), int(regime), float(dt),
+    return OraParams(_MODELS[model], int(k), int(rk_order), int(regime), float(dt),
                      float(dx), float(eps), float(speed), int(scheme), int(lf_order),
-                     int(m_eff), int(repeats))
+                     int(m_eff), int(repeats), float(gravity))
 
 
 def regime_for_shape(shape) -> int:
     """NumPy's candidate-sum order for advance(u) on an array of this shape:
     sequential when the leading axes hold >= 2 fields, 2-lane otherwise
-    (verified against the reference)."""
+    (verified against the reference).  (Systems use
+    the 2-lane order always; the oracle applies that internally.)"""
     n = int(np.prod(shape[:-2])) if len(shape) > 2 else 1
     return SUM_SEQ if n >= 2 else SUM_LANE2
 
 
 def phi_apply(params: OraParams, u: np.ndarray, g: np.ndarray | None = None,
               nthreads: int = 0) -> np.ndarray:
-    """Apply Phi (+ g) to every (1, N) field of u; shape preserved."""
+    """Apply Phi (+ g) to every (D, N) field of u; shape preserved."""
     u = np.ascontiguousarray(u, dtype=np.float64)
     nx = u.shape[-1]
-    batch = u.size // nx
+    row = nx * (2 if params.model == MODEL_SHALLOW_WATER else 1)
+    batch = u.size // row
     out = np.empty_like(u)
     gp = None
     if g is not None:
         g = np.ascontiguousarray(np.broadcast_to(g, u.shape), dtype=np.float64)
         gp = _ptr(g)
-    rc = lib().ora_phi_apply(ctypes.byref(params), _ptr(u), nx, gp, nx,
-                             _ptr(out), nx, batch, nx, int(nthreads))
+    rc = lib().ora_phi_apply(ctypes.byref(params), _ptr(u), row, gp, row,
+                             _ptr(out), row, batch, nx, int(nthreads))
+    if rc == 3:
+        raise PhysicalStateOracleError("non-positive depth")
     if rc != 0:
         raise ValueError(f"ora_phi_apply failed with status {rc}")
     return out
@@ -148,7 +160,8 @@ class OracleStepper:
 
     def __init__(self, *, model="burgers", k=2, rk_order=3, dt, dx,
                  eps=1e-6, speed=1.0, nthreads=0, scheme=0, lf_order=0, m_eff=1,
-                 repeats=1, formula_dt=None):
+                 repeats=1, formula_dt=None, gravity=9.81):
+        self.gravity = gravity
         self.model, self.k, self.order = model, k, rk_order
         self.dt, self.dx, self.eps, self.speed = dt, dx, eps, speed
         self.nthreads = nthreads
@@ -160,7 +173,7 @@ class OracleStepper:
                            dt=self.formula_dt, dx=self.dx, eps=self.eps,
                            speed=self.speed, regime=regime, scheme=self.scheme,
                            lf_order=self.lf_order, m_eff=self.m_eff,
-                           repeats=self.repeats)
+                           repeats=self.repeats, gravity=self.gravity)
 
     def advance(self, u):
         u = np.asarray(u, dtype=np.float64)

@@ -43,6 +43,7 @@
 
 #define ORA_MODEL_BURGERS 0
 #define ORA_MODEL_ADVECTION 1
+#define ORA_MODEL_SHALLOW_WATER 2   /* D = 2: (h, hu), characteristic WENO */
 #define ORA_SUM_SEQ 0
 #define ORA_SUM_LANE2 1
 
@@ -56,7 +57,10 @@ typedef struct {
     int32_t lf_order;  /* matched: 0 or 1                                     */
     int32_t m_eff;     /* matched: fine steps emulated                        */
     int32_t repeats;   /* composition count (ComposedStepper), >= 1           */
+    double gravity;    /* shallow water g                                     */
 } ora_params;
+
+static int ncomp(const ora_params *p) { return p->model == ORA_MODEL_SHALLOW_WATER ? 2 : 1; }
 
 /* ---- exact rational tables, weno.py:43-86.  IEEE division of the small
  * integers gives the correctly rounded double, i.e. float(Fraction(p, q)). */
@@ -155,23 +159,27 @@ static double recon(const ora_tables *t, int regime, const double *w) {
 }
 
 typedef struct {
-    int64_t nx;
+    int64_t nx;    /* cells */
+    int64_t len;   /* doubles per state: ncomp * nx */
     double *pad;   /* field with k+1 periodic halo cells on both sides */
     double *ul, *ur, *F, *A, *u1, *u2, *tmp;
+    int bad_state; /* PhysicalStateError: non-positive depth met */
 } ora_work;
 
-static int work_alloc(ora_work *w, int64_t nx, int k) {
+static int work_alloc(ora_work *w, int64_t nx, int k, int D) {
     w->nx = nx;
+    w->len = D * nx;
+    w->bad_state = 0;
     const int64_t H = k + 1;
-    w->pad = (double *)malloc(sizeof(double) * (size_t)(nx + 2 * H));
-    w->ul = (double *)malloc(sizeof(double) * (size_t)nx * 7);
+    w->pad = (double *)malloc(sizeof(double) * (size_t)(D * (nx + 2 * H)));
+    w->ul = (double *)malloc(sizeof(double) * (size_t)w->len * 7);
     if (!w->pad || !w->ul) { free(w->pad); free(w->ul); return 1; }
-    w->ur = w->ul + nx;
-    w->F = w->ur + nx;
-    w->A = w->F + nx;
-    w->u1 = w->A + nx;
-    w->u2 = w->u1 + nx;
-    w->tmp = w->u2 + nx;
+    w->ur = w->ul + w->len;
+    w->F = w->ur + w->len;
+    w->A = w->F + w->len;
+    w->u1 = w->A + w->len;
+    w->u2 = w->u1 + w->len;
+    w->tmp = w->u2 + w->len;
     return 0;
 }
 
@@ -247,6 +255,148 @@ static void rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
     }
 }
 
+/* ---- shallow water (models.py:136-211), characteristic WENO
+ * (weno.py:222-233), LF or Roe flux (flux.py:70-126).  State (h, hu),
+ * component-major rows of nx.  Checked against the reference bit for bit
+ * (tests/golden/make_golden.py): the characteristic windows are einsum
+ * outputs (contiguous), so the candidate sums always use the 2-lane order;
+ * the 2-term projections accumulate from +0 in index order. */
+static int sw_dv(ora_work *wk, double h, double hu, double *vel) {
+    if (h <= 0.0) wk->bad_state = 1;          /* PhysicalStateError */
+    *vel = hu / h;
+    return 0;
+}
+
+static void sw_eigen(ora_work *wk, double g, double h, double hu, double R[2][2], double L[2][2]) {
+    double vel;
+    sw_dv(wk, h, hu, &vel);
+    const double c = sqrt(g * h);
+    const double inv2c = 0.5 / c;
+    R[0][0] = 1.0; R[0][1] = 1.0; R[1][0] = vel - c; R[1][1] = vel + c;
+    L[0][0] = (vel + c) * inv2c; L[0][1] = -1.0 * inv2c;
+    L[1][0] = (-(vel - c)) * inv2c; L[1][1] = 1.0 * inv2c;
+}
+
+static void sw_flux(ora_work *wk, double g, const double *s, double *f) {
+    double vel;
+    sw_dv(wk, s[0], s[1], &vel);
+    f[0] = s[1];
+    f[1] = ((s[0] * vel) * vel) + (((0.5 * g) * s[0]) * s[0]);
+}
+
+static double sw_speed(ora_work *wk, double g, const double *s) {
+    double vel;
+    sw_dv(wk, s[0], s[1], &vel);
+    return fabs(vel) + sqrt(g * s[0]);
+}
+
+static double entropy_fix1(double lh, double ll, double lr) {
+    const double a = lh - ll, b = lr - lh;
+    const double inner = (a >= b || isnan(a)) ? a : b;
+    const double delta = (0.0 >= inner) ? 0.0 : inner;
+    const double alam = fabs(lh);
+    return (alam < delta) ? 0.5 * ((lh * lh) / delta + delta) : alam;
+}
+
+static void sw_rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
+                         const double *v, double *A) {
+    const int64_t nx = wk->nx;
+    const int k = t->k, W = 2 * k + 1;
+    const double g = p->gravity;
+    double *sl = wk->ul, *sr = wk->ur, *F = wk->F;   /* component-major (2, nx) */
+    for (int64_t i = 0; i < nx; ++i) {
+        double R0[2][2], L0[2][2], R1[2][2], L1[2][2];
+        const int64_t ip = (i + 1) % nx;
+        sw_eigen(wk, g, v[i], v[nx + i], R0, L0);
+        sw_eigen(wk, g, v[ip], v[nx + ip], R1, L1);
+        for (int side = 0; side < 2; ++side) {
+            double (*Lv)[2] = side == 0 ? L0 : L1;
+            double (*Rv)[2] = side == 0 ? R0 : R1;
+            double ch[2][7], rec[2];
+            for (int s2 = 0; s2 < W; ++s2) {
+                /* left window: cells i-k+s2; right window: cells i+1+k-s2 */
+                const int64_t c = side == 0 ? (i - k + s2) : (i + 1 + k - s2);
+                const int64_t cc = ((c % nx) + nx) % nx;
+                for (int q = 0; q < 2; ++q) {
+                    double acc = 0.0;
+                    acc = acc + Lv[q][0] * v[cc];
+                    acc = acc + Lv[q][1] * v[nx + cc];
+                    ch[q][s2] = acc;
+                }
+            }
+            for (int q = 0; q < 2; ++q) rec[q] = recon(t, ORA_SUM_LANE2, ch[q]);
+            double *dst = side == 0 ? sl : sr;
+            for (int d = 0; d < 2; ++d) {
+                double acc = 0.0;
+                acc = acc + Rv[d][0] * rec[0];
+                acc = acc + Rv[d][1] * rec[1];
+                dst[d * nx + i] = acc;
+            }
+        }
+    }
+    if (p->scheme == 3) {                       /* Roe, flux.py:91-126 */
+        for (int64_t i = 0; i < nx; ++i) {
+            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
+            double vl, vr;
+            sw_dv(wk, l[0], l[1], &vl);
+            sw_dv(wk, r[0], r[1], &vr);
+            const double s_l = sqrt(l[0]), s_r = sqrt(r[0]);
+            const double hh = 0.5 * (l[0] + r[0]);
+            const double uh = (s_l * vl + s_r * vr) / (s_l + s_r);
+            const double ch = sqrt(g * hh);
+            const double lam[2] = {uh - ch, uh + ch};
+            const double inv2c = 0.5 / ch;
+            const double Rr[2][2] = {{1.0, 1.0}, {lam[0], lam[1]}};
+            const double Lr[2][2] = {{(uh + ch) * inv2c, -1.0 * inv2c},
+                                     {(-(uh - ch)) * inv2c, 1.0 * inv2c}};
+            const double jump[2] = {r[0] - l[0], r[1] - l[1]};
+            const double cl = sqrt(g * l[0]), cr = sqrt(g * r[0]);
+            const double ll[2] = {vl - cl, vl + cl}, lr[2] = {vr - cr, vr + cr};
+            double ss[2];
+            for (int kk = 0; kk < 2; ++kk) {
+                double acc = 0.0;
+                acc = acc + Lr[kk][0] * jump[0];
+                acc = acc + Lr[kk][1] * jump[1];
+                ss[kk] = entropy_fix1(lam[kk], ll[kk], lr[kk]) * acc;
+            }
+            double fl[2], fr[2];
+            sw_flux(wk, g, l, fl);
+            sw_flux(wk, g, r, fr);
+            for (int d = 0; d < 2; ++d) {
+                double acc = 0.0;
+                acc = acc + ss[0] * Rr[d][0];
+                acc = acc + ss[1] * Rr[d][1];
+                F[d * nx + i] = (0.5 * (fl[d] + fr[d])) - (0.5 * acc);
+            }
+        }
+    } else {                                    /* global LF, flux.py:70-88 */
+        double ml = 0.0, mr = 0.0;
+        int nan = 0;
+        for (int64_t i = 0; i < nx; ++i) {
+            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
+            const double a = sw_speed(wk, g, l), b = sw_speed(wk, g, r);
+            if (isnan(a) || isnan(b)) nan = 1;
+            if (a > ml) ml = a;
+            if (b > mr) mr = b;
+        }
+        const double alpha = nan ? NAN : (ml > mr ? ml : mr);
+        const double ha = 0.5 * alpha;
+        for (int64_t i = 0; i < nx; ++i) {
+            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
+            double fl[2], fr[2];
+            sw_flux(wk, g, l, fl);
+            sw_flux(wk, g, r, fr);
+            for (int d = 0; d < 2; ++d)
+                F[d * nx + i] = (0.5 * (fl[d] + fr[d])) - (ha * (r[d] - l[d]));
+        }
+    }
+    for (int d = 0; d < 2; ++d)
+        for (int64_t i = 0; i < nx; ++i) {
+            const double fm = F[d * nx + (i == 0 ? nx - 1 : i - 1)];
+            A[d * nx + i] = (-(F[d * nx + i] - fm)) / p->dx;
+        }
+}
+
 /* E(u)_i = 0.5 (u_{i+1} + u_{i-1})  (stepper.py:85-87) */
 static void ora_E(const double *u, double *out, int64_t n) {
     for (int64_t i = 0; i < n; ++i)
@@ -303,7 +453,7 @@ static void phi_once(const ora_params *p, const ora_tables *t, ora_work *wk,
 /* ComposedStepper (stepper.py:170-188): inner^repeats, then "+ g" */
 static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
                       const double *u, const double *g, double *out) {
-    const int64_t nx = wk->nx;
+    const int64_t nx = wk->len;
     phi_once(p, t, wk, u, out);
     for (int r = 1; r < p->repeats; ++r) {
         memcpy(wk->tmp, out, sizeof(double) * (size_t)nx);
@@ -313,36 +463,42 @@ static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
         for (int64_t i = 0; i < nx; ++i) out[i] = out[i] + g[i];
 }
 
+static void any_rhs(const ora_params *p, const ora_tables *t, ora_work *wk,
+                    const double *v, double *A) {
+    if (p->model == ORA_MODEL_SHALLOW_WATER) sw_rhs_field(p, t, wk, v, A);
+    else rhs_field(p, t, wk, v, A);
+}
+
 static void phi_once(const ora_params *p, const ora_tables *t, ora_work *wk,
                      const double *u, double *out) {
-    const int64_t nx = wk->nx;
+    const int64_t nx = wk->len;   /* elementwise RK over every component */
     double *A = wk->A, *u1 = wk->u1, *u2 = wk->u2;
     if (p->scheme == 1 || p->scheme == 2) {
         lf_field(p, wk, u, out);
         return;
     }
     if (p->rk_order == 0) {
-        rhs_field(p, t, wk, u, out);
+        any_rhs(p, t, wk, u, out);
         return;
     }
     const double dt = p->dt;
-    rhs_field(p, t, wk, u, A);
+    any_rhs(p, t, wk, u, A);
     for (int64_t i = 0; i < nx; ++i) u1[i] = u[i] + dt * A[i];
     if (p->rk_order == 1) {
         for (int64_t i = 0; i < nx; ++i) out[i] = u1[i];
     } else if (p->rk_order == 2) {
         const double hdt = 0.5 * dt;
-        rhs_field(p, t, wk, u1, A);
+        any_rhs(p, t, wk, u1, A);
         for (int64_t i = 0; i < nx; ++i)
             out[i] = ((0.5 * u[i]) + (0.5 * u1[i])) + (hdt * A[i]);
     } else {
         const double qdt = 0.25 * dt;
         const double two3 = 2.0 / 3.0;
         const double tdt = two3 * dt;
-        rhs_field(p, t, wk, u1, A);
+        any_rhs(p, t, wk, u1, A);
         for (int64_t i = 0; i < nx; ++i)
             u2[i] = ((0.75 * u[i]) + (0.25 * u1[i])) + (qdt * A[i]);
-        rhs_field(p, t, wk, u2, A);
+        any_rhs(p, t, wk, u2, A);
         for (int64_t i = 0; i < nx; ++i)
             out[i] = ((u[i] / 3.0) + (two3 * u2[i])) + (tdt * A[i]);
     }
@@ -354,10 +510,11 @@ static int check_params(const ora_params *p, int64_t nx) {
         return (p->model != ORA_MODEL_BURGERS || nx < 1 ||
                 (p->scheme == 2 && (p->m_eff < 1 || p->lf_order < 0 || p->lf_order > 1)));
     if (p->scheme != 0 && p->scheme != 3) return 1;
-    if (p->scheme == 3 && p->model != ORA_MODEL_BURGERS) return 1;
+    if (p->scheme == 3 && p->model == ORA_MODEL_ADVECTION) return 1;
+    if (p->model == ORA_MODEL_SHALLOW_WATER && !(p->gravity > 0.0)) return 1;
     if (p->k < 0 || p->k > 3) return 1;
     if (p->rk_order < 0 || p->rk_order > 3) return 1;
-    if (p->model != ORA_MODEL_BURGERS && p->model != ORA_MODEL_ADVECTION) return 1;
+    if (p->model < ORA_MODEL_BURGERS || p->model > ORA_MODEL_SHALLOW_WATER) return 1;
     if (p->regime != ORA_SUM_SEQ && p->regime != ORA_SUM_LANE2) return 1;
     if (nx < 2 * p->k + 1) return 1;
     return 0;
@@ -373,12 +530,13 @@ typedef struct {
     int64_t next;
     pthread_mutex_t lock;
     int err;
+    int bad;
 } ora_job;
 
 static void *ora_worker(void *arg) {
     ora_job *job = (ora_job *)arg;
     ora_work wk;
-    if (work_alloc(&wk, job->nx, job->p->k)) {
+    if (work_alloc(&wk, job->nx, job->p->k, ncomp(job->p))) {
         pthread_mutex_lock(&job->lock);
         job->err = 1;
         pthread_mutex_unlock(&job->lock);
@@ -393,6 +551,11 @@ static void *ora_worker(void *arg) {
                   job->g ? job->g + b * job->g_stride : NULL,
                   job->out + b * job->out_stride);
     }
+    if (wk.bad_state) {
+        pthread_mutex_lock(&job->lock);
+        job->bad = 1;
+        pthread_mutex_unlock(&job->lock);
+    }
     work_free(&wk);
     return NULL;
 }
@@ -406,8 +569,9 @@ int ora_max_threads(void) {
  * out[b] = Phi(u[b]) (+ g[b] when g != NULL) for b < batch; rows of nx
  * doubles with the given strides (in elements).  u_stride 0 broadcasts one
  * state.  Fields are independent and are spread over nthreads POSIX threads
- * (nthreads <= 0: one per online core).  Returns 0, 1 on bad arguments, 2 on
- * allocation failure.
+ * (nthreads <= 0: one per online core).  Rows hold ncomp(model) * nx doubles
+ * (component-major).  Returns 0, 1 on bad arguments, 2 on allocation failure,
+ * 3 when a non-positive depth was met (the reference's PhysicalStateError).
  */
 int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
                   const double *g, int64_t g_stride, double *out,
@@ -418,10 +582,10 @@ int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
     if (nthreads <= 0) nthreads = ora_max_threads();
     if (nthreads > batch) nthreads = batch > 0 ? (int)batch : 1;
     ora_job job = {p, &t, u, g, out, u_stride, g_stride, out_stride, batch, nx,
-                   0, PTHREAD_MUTEX_INITIALIZER, 0};
+                   0, PTHREAD_MUTEX_INITIALIZER, 0, 0};
     if (nthreads == 1) {
         ora_worker(&job);
-        return job.err ? 2 : 0;
+        return job.err ? 2 : (job.bad ? 3 : 0);
     }
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
     if (!th) return 2;
@@ -431,7 +595,7 @@ int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
     if (started == 0) ora_worker(&job);
     for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
     free(th);
-    return job.err ? 2 : 0;
+    return job.err ? 2 : (job.bad ? 3 : 0);
 }
 
 /*
@@ -445,9 +609,11 @@ int ora_march(const ora_params *p, double *u, const double *g, int64_t n_steps,
     ora_tables t;
     build_tables(p->k, p->eps, &t);
     ora_work wk;
-    if (work_alloc(&wk, nx, p->k)) return 2;
+    if (work_alloc(&wk, nx, p->k, ncomp(p))) return 2;
+    const int64_t len = wk.len;
     for (int64_t i = 1; i <= n_steps; ++i)
-        phi_field(p, &t, &wk, u + (i - 1) * nx, g ? g + i * nx : NULL, u + i * nx);
+        phi_field(p, &t, &wk, u + (i - 1) * len, g ? g + i * len : NULL, u + i * len);
+    const int bad = wk.bad_state;
     work_free(&wk);
-    return 0;
+    return bad ? 3 : 0;
 }
