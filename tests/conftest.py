@@ -39,3 +39,19 @@ def gpu_available():
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+@pytest.fixture(scope="session")
+def sw_golden():
+    with open(os.path.join(GOLDEN, "sw_vectors.json")) as f:
+        index = json.load(f)
+    data = np.load(os.path.join(GOLDEN, "sw_vectors.npz"))
+    return index, data
+
+
+@pytest.fixture(scope="session")
+def sw_mgrit_golden():
+    with open(os.path.join(GOLDEN, "sw_mgrit_cases.json")) as f:
+        meta = json.load(f)
+    data = np.load(os.path.join(GOLDEN, "sw_mgrit_cases.npz"))
+    return {m["name"]: m for m in meta}, data

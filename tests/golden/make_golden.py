@@ -449,9 +449,142 @@ def lf_mgrit_cases():
         json.dump(meta, f, indent=1)
 
 
+# ---------------------------------------------------------------------------
+# shallow-water system (models.py:130-230, characteristic WENO flux.py:127-161)
+# -- SURVEY.md 8(f) rank 4
+# ---------------------------------------------------------------------------
+
+def sw_fields(rng, shape, kind):
+    nx = shape[-1]
+    x = (np.arange(nx) + 0.5) / nx
+    lead = shape[:-2]
+    u = np.empty(shape)
+    u[..., 0, :] = 0.1 + 0.05 * np.sin(2 * np.pi * x) + 0.01 * rng.random(lead + (nx,))
+    u[..., 1, :] = 0.02 * rng.standard_normal(lead + (nx,))
+    if kind == "bore":
+        u[..., 0, :] += np.where(x > 0.5, 0.0, 0.08)
+    elif kind == "nan":
+        u[..., 1, nx // 3] = np.nan
+    elif kind == "dry":      # non-positive depth -> PhysicalStateError
+        u[..., 0, 5] = -0.01
+    return np.ascontiguousarray(u)
+
+
+def sw_vectors():
+    rng = np.random.default_rng(4)
+    out, index = {}, []
+    nx = 32
+    sg = R.SpatialGrid(1.0, nx)
+    model = R.make_model("shallow-water")
+    dt = 0.2 * sg.dx
+    n = 0
+    for flux in ("lf", "roe"):
+        for k in (0, 1, 2, 3):
+            op = R.SemiDiscreteOperator(model, sg, R.FluxConfig(flux, R.WenoConfig(2 * k + 1)))
+            for rk in (0, 1, 2, 3):
+                st = R.RungeKuttaStepper(op.rhs, dt, max(rk, 1))
+                for shape in ((3, 2, nx), (2, nx)):
+                    kinds = ["smooth", "bore"]
+                    if rk == 3 and len(shape) == 3:
+                        kinds += ["nan", "dry"]
+                    for fk in kinds:
+                        u = sw_fields(rng, shape, fk)
+                        p = oracle.make_params(model="shallow-water", k=k, rk_order=rk,
+                                               dt=dt, dx=sg.dx, regime=oracle.SUM_LANE2,
+                                               scheme=3 if flux == "roe" else 0)
+                        try:
+                            with np.errstate(all="ignore"):
+                                y = op.rhs(u) if rk == 0 else st.advance(u)
+                            raised = False
+                        except R.PhysicalStateError:
+                            y, raised = np.full_like(u, np.nan), True
+                        try:
+                            mine = oracle.phi_apply(p, u)
+                            assert not raised, (flux, k, rk, fk)
+                            assert np.array_equal(mine, y, equal_nan=True), (flux, k, rk, shape, fk)
+                        except oracle.PhysicalStateOracleError:
+                            assert raised, (flux, k, rk, fk)
+                        key = f"sw{n:03d}"
+                        out[key + "_in"], out[key + "_out"] = u, y
+                        index.append(dict(key=key, flux=flux, k=k, rk=rk, shape=list(shape),
+                                          field=fk, dt=dt, dx=sg.dx, gravity=model.gravity,
+                                          raises=raised))
+                        n += 1
+    np.savez_compressed(os.path.join(HERE, "sw_vectors.npz"), **out)
+    with open(os.path.join(HERE, "sw_vectors.json"), "w") as f:
+        json.dump(index, f, indent=0)
+    print(f"sw vectors: {len(index)}")
+
+
+SW_CONFIGS = ["high_order_shallow_water_lf.cfg", "high_order_shallow_water_roe.cfg"]
+
+
+def sw_mgrit_cases():
+    arrays, meta = {}, []
+    cfg_dir = "/root/reference/pkg/configs"
+    from mgritlab.harness import build_steppers as ref_build_steppers
+    for fname in SW_CONFIGS:
+        base = R.load_config(os.path.join(cfg_dir, fname))
+        for raw in base.sweep_values:
+            col = R.apply_sweep_value(dataclasses.replace(base, sweep=None, sweep_values=()),
+                                      base.sweep, raw)
+            res = R.run_experiment(col)
+            sg = R.SpatialGrid(col.length, col.n_x)
+            tg = R.TemporalGrid(col.horizon, col.n_t)
+            u0 = R.initial_state(col.ic, sg, col.length)
+            steppers = ref_build_steppers(col, R.make_model(col.problem), sg, tg)
+            ost = []
+            for st in steppers:
+                op = st.rhs.__self__
+                ost.append(oracle.OracleStepper(
+                    model="shallow-water", k=op.config.weno.degree, rk_order=st.order,
+                    dt=st.dt, dx=sg.dx, eps=op.config.weno.epsilon, nthreads=1,
+                    scheme=3 if op.config.kind == "roe" else 0,
+                    gravity=op.model.gravity))
+            oref = mgrit_oracle.march(ost[0], u0, col.n_t)
+            o_opts = mgrit_oracle.Options(n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                                          relaxation=col.relaxation,
+                                          guess=col.restriction_guess,
+                                          max_iters=col.max_iters)
+            otraj, orec = mgrit_oracle.mgrit_solve(ost, u0, col.n_t, tg.dt, o_opts,
+                                                   reference=oref)
+            opts = R.MgritOptions(n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                                  relaxation=col.relaxation, guess=col.restriction_guess,
+                                  max_iters=col.max_iters)
+            traj, rec = R.mgrit_solve(steppers, u0, tg, sg, opts,
+                                      reference=res.serial.trajectory.values)
+            assert np.array_equal(rec.errors, res.record.errors, equal_nan=True), fname
+            assert np.array_equal(oref, res.serial.trajectory.values), fname
+            assert orec.diverged_at == res.record.diverged_at, fname
+            ok = np.isfinite(res.record.errors)
+            assert np.allclose(orec.errors[ok], res.record.errors[ok], rtol=1e-12), fname
+            assert np.array_equal(otraj, traj.values, equal_nan=True), fname
+            name = fname[:-4] + "__" + str(raw)
+            arrays[name + "__u0"] = u0
+            arrays[name + "__errors"] = res.record.errors
+            arrays[name + "__residuals"] = res.record.residuals
+            arrays[name + "__traj"] = traj.values
+            meta.append(dict(name=name, model="shallow-water", n_x=col.n_x, n_t=col.n_t,
+                             flux=col.flux, horizon=col.horizon, dt=tg.dt, length=col.length,
+                             stepper=list(col.stepper), weno_order=list(col.weno_order),
+                             coarse=col.coarse, n_levels=col.n_levels, m=col.m,
+                             cycle=col.cycle, relaxation=col.relaxation,
+                             guess=col.restriction_guess, max_iters=col.max_iters,
+                             gravity=R.make_model(col.problem).gravity, ic=col.ic,
+                             semantics="harness", diverged_at=res.record.diverged_at,
+                             has_traj=True))
+            print(f"{name}: diverged_at={res.record.diverged_at} err={res.record.errors}")
+    np.savez_compressed(os.path.join(HERE, "sw_mgrit_cases.npz"), **arrays)
+    with open(os.path.join(HERE, "sw_mgrit_cases.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 if __name__ == "__main__":
     import sys as _sys
-    which = _sys.argv[1:] or ["phi", "mgrit", "lf"]
+    which = _sys.argv[1:] or ["phi", "mgrit", "lf", "sw"]
+    if "sw" in which:
+        sw_vectors()
+        sw_mgrit_cases()
     if "phi" in which:
         phi_vectors()
     if "mgrit" in which:
