@@ -24,7 +24,9 @@
  *                       grid.py:105-108) and np.isfinite (mgrit.py:323).
  *
  * Conventions: all pointers are device pointers owned by the caller; states
- * are rows of `nx` float64 cells; strides are in elements (float64), may be
+ * are rows of D*nx float64 values (D = 1 for the scalar models; D = 2 for
+ * shallow water, component-major: nx depths h then nx momenta hu, the
+ * reference's (..., D, N) layout); strides are in elements (float64), may be
  * 0 to broadcast one row.  Every call is asynchronous on `stream`
  * (a cudaStream_t, NULL = legacy default stream).  Return codes: MGP_OK,
  * MGP_EINVAL (bad argument: the Python layer raises ConfigError, mirroring
@@ -49,6 +51,14 @@ extern "C" {
  * config 1 needs (flux a*u, |lambda| = |a|). */
 #define MGP_MODEL_BURGERS 0
 #define MGP_MODEL_ADVECTION 1
+/* ShallowWater (models.py:136-211): state (h, hu), flux (hu, h u^2 + g h^2/2),
+ * characteristic WENO (weno.py:222-233) with the LF or Roe flux; rows of
+ * 2*nx, nx <= 2048, candidate sums always in the 2-lane order (the
+ * characteristic windows are fresh contiguous arrays in the reference). */
+#define MGP_MODEL_SHALLOW_WATER 2
+
+/* bits OR-ed into *mgp_sweep_args.status where the reference raises */
+#define MGP_STATUS_NONPOSITIVE_DEPTH 1   /* PhysicalStateError, models.py:147-153 */
 
 /* NumPy candidate-sum order of weno.py:175:
  * SEQ when advance() received >= 2 fields, LANE2 for a single field. */
@@ -97,6 +107,7 @@ typedef struct mgp_phi {
     int32_t m_eff;      /* MGP_SCHEME_LF_MATCHED: fine steps emulated (m^l)    */
     int32_t repeats;    /* >= 1: Phi = inner^repeats (ComposedStepper,
                            stepper.py:170-188); 1 otherwise                    */
+    double gravity;     /* shallow water: g > 0 (models.py:139-143)            */
 } mgp_phi;
 
 /*
@@ -149,6 +160,10 @@ typedef struct mgp_sweep_args {
     int32_t ref_last_next;
     int32_t count_nonfinite;
     double *partials;
+    int32_t *status;      /* optional device word: MGP_STATUS_* bits are OR-ed
+                             in when a state the reference rejects is met
+                             (the sweep still completes; the caller checks the
+                             word after synchronising and raises) */
 } mgp_sweep_args;
 
 int mgp_sweep(const mgp_sweep_args *args, void *stream);
@@ -160,7 +175,8 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width,
 
 /* Largest nx supported for a propagator: 4096 cells per CTA (whole field in
  * shared memory); WENO5 Burgers fields up to 16 x 4096 cells are split over a
- * thread-block cluster (nx must then divide into power-of-two slabs). */
+ * thread-block cluster (nx must then divide into power-of-two slabs);
+ * shallow water 2048 cells. */
 int64_t mgp_max_nx(int32_t weno_k, int32_t model);
 
 /* Library/ABI version and the compile-time WENO tables of degree k, written

@@ -27,6 +27,9 @@ G_NONE, G_ZERO, G_ARRAY = 0, 1, 2
 TAIL_NONE, TAIL_PHI, TAIL_RESTRICT, TAIL_RESID = 0, 1, 2, 3
 SCHEME_RK_WENO, SCHEME_LF_ONESTEP, SCHEME_LF_MATCHED, SCHEME_RK_WENO_ROE = 0, 1, 2, 3
 GUESS_LAST_STEP, GUESS_INJECTION = 0, 1
+MODEL_BURGERS, MODEL_ADVECTION, MODEL_SHALLOW_WATER = 0, 1, 2
+STATUS_NONPOSITIVE_DEPTH = 1
+ABI_VERSION = 2
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -45,7 +48,7 @@ class MgpPhi(ctypes.Structure):
                 ("dx", ctypes.c_double), ("epsilon", ctypes.c_double),
                 ("speed", ctypes.c_double), ("scheme", ctypes.c_int32),
                 ("lf_order", ctypes.c_int32), ("m_eff", ctypes.c_int32),
-                ("repeats", ctypes.c_int32)]
+                ("repeats", ctypes.c_int32), ("gravity", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -72,6 +75,7 @@ class MgpSweepArgs(ctypes.Structure):
         ("ref_last_next", _I32),
         ("count_nonfinite", _I32),
         ("partials", _P),
+        ("status", _P),
     ]
 
 
@@ -131,6 +135,14 @@ def check(rc: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(load().mgp_launch_count())
+
+
+def max_nx_static(weno_k: int = 2, model: int = 0) -> int:
+    """The library's mesh limits (mgp_max_nx) without loading it: 4096 cells
+    per CTA, WENO5 Burgers up to 16 x 4096 over a cluster, shallow water 2048."""
+    if model == MODEL_SHALLOW_WATER:
+        return 2048
+    return 16 * 4096 if (weno_k == 2 and model == MODEL_BURGERS) else 4096
 
 
 def max_nx(weno_k: int = 2, model: int = 0) -> int:

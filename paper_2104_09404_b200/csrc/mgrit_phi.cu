@@ -127,7 +127,7 @@ constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
 
 // kernel-internal model id: Burgers with the Roe flux (mgp_phi.scheme ==
 // MGP_SCHEME_RK_WENO_ROE), no global alpha, NaN kept local like the reference
-constexpr int kModelBurgersRoe = 2;
+constexpr int kModelBurgersRoe = 8;
 
 #ifndef MGP_SLIDE_UNROLL
 #define MGP_SLIDE_UNROLL 1
@@ -290,6 +290,7 @@ struct Consts {
     double twodx, inv_twodx;   // one-step LF family: central difference 2 dx
     int dx_pow2, twodx_pow2;
     int lf_order, m_eff;
+    double gravity;            // shallow water
 };
 
 namespace cg = cooperative_groups;
@@ -654,8 +655,8 @@ __device__ __forceinline__ double g_value(int mode, const double *g, int c) {
 template <class F, int CS>
 __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts &k, F &f,
                                            const int ns, const int q, const int c0,
-                                           double *s_sum, double *s_psum) {
-    const int nx = (int)a.phi.nx;
+                                           double *s_sum, double *s_psum, const int nx) {
+    // nx: row length in elements (periodic wrap of the halo loads)
     const int tid = threadIdx.x, nt = blockDim.x;
     const int rk = a.phi.rk_order;
     const int total = a.n_steps + (a.tail != MGP_TAIL_NONE ? 1 : 0);
@@ -798,7 +799,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     const int ns = nx / CS;            // cells of this CTA's slab
     const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
     const int c0 = q * ns;             // global index of local cell 0
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int tid = threadIdx.x;
     f.ns = ns;
     f.q = q;
     f.run = tid;
@@ -818,7 +819,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
         f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
         f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
     }
-    sweep_body<F, CS>(a, k, f, ns, q, c0, s_sum, s_psum);
+    sweep_body<F, CS>(a, k, f, ns, q, c0, s_sum, s_psum, nx);
 }
 
 // ---------------------------------------------------------------------------
@@ -912,7 +913,270 @@ __global__ void __launch_bounds__(256) lf_kernel(const mgp_sweep_args a, const C
     f.s_f = f.s_ab + nx;
     double *s_sum = f.s_f + nx;
     double *s_psum = s_sum + 3 * 32;
-    sweep_body<LFField<MODE>, 1>(a, k, f, nx, 0, 0, s_sum, s_psum);
+    sweep_body<LFField<MODE>, 1>(a, k, f, nx, 0, 0, s_sum, s_psum, nx);
+}
+
+// ---------------------------------------------------------------------------
+// Shallow-water system (models.py:136-211): state (h, hu), component-major
+// rows of 2 nx.  Characteristic WENO (weno.py:222-233, flux.py:127-161): the
+// window of cell c is projected onto the left eigenvectors of cell c,
+//   L(c) = [[(u+c)/2c, -1/2c], [-(u-c)/2c, 1/2c]],  c = sqrt(g h),
+// each characteristic field is reconstructed (left state of interface c and
+// right state of interface c-1 from the same window, shared beta products),
+// and mapped back with R(c) = [[1, 1], [u-c, u+c]].  The einsum projections
+// accumulate from +0 in index order; the candidate sums use the 2-lane order
+// (the characteristic windows are contiguous arrays in the reference).  Flux:
+// global LF (alpha = NaN-propagating max of |u| + sqrt(g h) over both
+// interface states) or Roe with the Harten-Hyman entropy fix per
+// characteristic field (flux.py:91-126, models.py:185-211).  Depth <= 0 in any
+// state the reference passes through _depth_velocity raises
+// PhysicalStateError there (models.py:147-153); here it sets
+// MGP_STATUS_NONPOSITIVE_DEPTH in *status and the sweep completes.
+// One CTA per field, whole field in shared memory (nx <= kMaxSysNx).
+// ---------------------------------------------------------------------------
+constexpr int kMaxSysNx = 2048;
+
+__device__ __forceinline__ double entropy_fix(double lh, double ll, double lr) {
+    const double a = lh - ll, b = lr - lh;
+    const double inner = (a >= b || a != a) ? a : b;      // np.maximum
+    const double delta = (0.0 >= inner) ? 0.0 : inner;
+    const double alam = fabs(lh);
+    return (alam < delta) ? 0.5 * ((lh * lh) / delta + delta) : alam;
+}
+
+template <int K, bool ROE>
+struct SysField {
+    static constexpr int HALO = 0;   // halos are maintained by load/put
+    static constexpr int H = K;      // window reach
+    int nx, pitch;                   // cells; per-component stride of s_u
+    double *s_u;    // stage input: component d, cell c at s_u[d*pitch + H + c]
+    double *s_u0;   // RK base, element e = d*nx + c
+    double *s_L;    // left states at interface i (e = d*nx + i), then fluxes
+    double *s_R;    // right states at interface i, then results
+    unsigned long long *s_red;   // [32] per-warp alpha bits
+    int32_t *status;
+    bool bad;
+
+    __device__ __forceinline__ double cellv(int d, int c) const {
+        return s_u[d * pitch + H + c];
+    }
+    __device__ __forceinline__ void load(int e, double v) {
+        const int d = e >= nx ? 1 : 0;
+        const int c = e - d * nx;
+        double *row = s_u + d * pitch + H;
+        row[c] = v;
+        if (c < H) row[nx + c] = v;
+        if (c >= nx - H) row[c - nx] = v;
+    }
+    __device__ __forceinline__ void put(int e, double v) { load(e, v); }
+    __device__ __forceinline__ double result(int e) const { return s_R[e]; }
+    __device__ __forceinline__ void sync() { __syncthreads(); }
+
+    __device__ __forceinline__ void check(double h) {
+        if (h <= 0.0) bad = true;
+    }
+
+    // WENO of one characteristic window: left state (interface m) and right
+    // state (interface m-1)
+    __device__ __forceinline__ void recon2(const Consts &k, const double *w, double &l,
+                                           double &r) const {
+        double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
+#pragma unroll
+        for (int s2 = 0; s2 <= K; ++s2) beta_block<K, true>(w, s2, bl[s2], br[K - s2]);
+#pragma unroll
+        for (int q = 0; q <= K; ++q) {
+            ql[q] = cand_left<K, MGP_SUM_LANE2>(w, q);
+            qr[q] = cand_right<K, MGP_SUM_LANE2>(w, q);
+        }
+        l = weno_value<K>(bl, ql, k.eps);
+        r = weno_value<K>(br, qr, k.eps);
+    }
+
+    // physical flux and |u| + sqrt(g h) of one interface state
+    __device__ __forceinline__ void flux(const Consts &k, double h, double hu, double &f0,
+                                         double &f1) {
+        check(h);
+        const double vel = hu / h;
+        f0 = hu;
+        f1 = ((h * vel) * vel) + (((0.5 * k.gravity) * h) * h);
+    }
+
+    // interface states of every interface; returns this thread's alpha bits
+    __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
+        unsigned long long m = 0;
+        const double g = k.gravity;
+        for (int c = threadIdx.x; c < nx; c += blockDim.x) {
+            const double h = cellv(0, c), hu = cellv(1, c);
+            check(h);
+            const double vel = hu / h;
+            const double cs = sqrt(g * h);
+            const double inv2c = 0.5 / cs;
+            const double L00 = (vel + cs) * inv2c, L01 = -1.0 * inv2c;
+            const double L10 = (-(vel - cs)) * inv2c, L11 = 1.0 * inv2c;
+            const double R10 = vel - cs, R11 = vel + cs;
+            double w0[2 * K + 1], w1[2 * K + 1];
+#pragma unroll
+            for (int s2 = 0; s2 <= 2 * K; ++s2) {
+                const double x0 = cellv(0, c - K + s2), x1 = cellv(1, c - K + s2);
+                double a0 = 0.0;
+                a0 = a0 + L00 * x0;
+                w0[s2] = a0 + L01 * x1;
+                double a1 = 0.0;
+                a1 = a1 + L10 * x0;
+                w1[s2] = a1 + L11 * x1;
+            }
+            double l0, r0, l1, r1;
+            recon2(k, w0, l0, r0);
+            recon2(k, w1, l1, r1);
+            // back to conserved variables: R(c) @ (rec0, rec1)
+            double t;
+            t = 0.0;
+            t = t + 1.0 * l0;
+            const double lh = t + 1.0 * l1;
+            t = 0.0;
+            t = t + R10 * l0;
+            const double lhu = t + R11 * l1;
+            t = 0.0;
+            t = t + 1.0 * r0;
+            const double rh = t + 1.0 * r1;
+            t = 0.0;
+            t = t + R10 * r0;
+            const double rhu = t + R11 * r1;
+            const int im = c == 0 ? nx - 1 : c - 1;
+            s_L[c] = lh;
+            s_L[nx + c] = lhu;
+            s_R[im] = rh;
+            s_R[nx + im] = rhu;
+            if (!ROE) {
+                check(lh);
+                check(rh);
+                const double sl = fabs(lhu / lh) + sqrt(g * lh);
+                const double sr = fabs(rhu / rh) + sqrt(g * rh);
+                m = umax64(m, umax64(abs_bits(sl), abs_bits(sr)));
+            }
+        }
+        return m;
+    }
+
+    __device__ __forceinline__ void rhs(const Consts &k, int last_stage_unused) {
+        unsigned long long m = reconstruct(k);
+        double half_alpha = 0.0;
+        if (!ROE) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = umax64(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+        }
+        __syncthreads();
+        if (!ROE) {
+            m = s_red[0];
+            const int nw = (blockDim.x + 31) >> 5;
+            for (int w = 1; w < nw; ++w) m = umax64(m, s_red[w]);
+            half_alpha = 0.5 * __longlong_as_double((long long)m);
+        }
+        const double g = k.gravity;
+        for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+            const double lh = s_L[i], lhu = s_L[nx + i];
+            const double rh = s_R[i], rhu = s_R[nx + i];
+            double fl0, fl1, fr0, fr1;
+            if (ROE) {
+                check(lh);
+                check(rh);
+                const double vl = lhu / lh, vr = rhu / rh;
+                const double sql = sqrt(lh), sqr = sqrt(rh);
+                const double hh = 0.5 * (lh + rh);
+                const double uh = (sql * vl + sqr * vr) / (sql + sqr);
+                const double ch = sqrt(g * hh);
+                const double lam0 = uh - ch, lam1 = uh + ch;
+                const double inv2c = 0.5 / ch;
+                const double Lr00 = (uh + ch) * inv2c, Lr01 = -1.0 * inv2c;
+                const double Lr10 = (-(uh - ch)) * inv2c, Lr11 = 1.0 * inv2c;
+                const double j0 = rh - lh, j1 = rhu - lhu;
+                const double cl = sqrt(g * lh), cr = sqrt(g * rh);
+                double t = 0.0;
+                t = t + Lr00 * j0;
+                t = t + Lr01 * j1;
+                const double ss0 = entropy_fix(lam0, vl - cl, vr - cr) * t;
+                t = 0.0;
+                t = t + Lr10 * j0;
+                t = t + Lr11 * j1;
+                const double ss1 = entropy_fix(lam1, vl + cl, vr + cr) * t;
+                flux(k, lh, lhu, fl0, fl1);
+                flux(k, rh, rhu, fr0, fr1);
+                t = 0.0;
+                t = t + ss0 * 1.0;
+                const double d0 = t + ss1 * 1.0;
+                t = 0.0;
+                t = t + ss0 * lam0;
+                const double d1 = t + ss1 * lam1;
+                s_L[i] = (0.5 * (fl0 + fr0)) - (0.5 * d0);
+                s_L[nx + i] = (0.5 * (fl1 + fr1)) - (0.5 * d1);
+            } else {
+                flux(k, lh, lhu, fl0, fl1);
+                flux(k, rh, rhu, fr0, fr1);
+                s_L[i] = (0.5 * (fl0 + fr0)) - (half_alpha * (rh - lh));
+                s_L[nx + i] = (0.5 * (fl1 + fr1)) - (half_alpha * (rhu - lhu));
+            }
+        }
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ double A(const Consts &k, int e) const {
+        const int d = e >= nx ? 1 : 0;
+        const int c = e - d * nx;
+        const double fm = s_L[d * nx + (c == 0 ? nx - 1 : c - 1)];
+        const double neg = -(s_L[e] - fm);
+        return k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+    }
+
+    __device__ void phi(const Consts &k, int rk) {
+        const int tid = threadIdx.x, nt = blockDim.x, n2 = 2 * nx;
+        bad = false;
+        for (int e = tid; e < n2; e += nt) s_u0[e] = cellv(e >= nx, e - (e >= nx) * nx);
+        const int stages = rk == 0 ? 1 : rk;
+#pragma unroll 1
+        for (int sg = 0; sg < stages; ++sg) {
+            if (sg > 0) __syncthreads();   // committed stage values visible
+            rhs(k, 0);
+            const bool last = (sg == stages - 1);
+            for (int e = tid; e < n2; e += nt) {
+                const double a = A(k, e);
+                const double u0 = s_u0[e];
+                double st;
+                if (rk == 0) {
+                    st = a;
+                } else if (sg == 0) {
+                    st = u0 + k.dt * a;
+                } else {
+                    const double cur = cellv(e >= nx, e - (e >= nx) * nx);
+                    if (rk == 2) st = ((0.5 * u0) + (0.5 * cur)) + (k.hdt * a);
+                    else if (sg == 1) st = ((0.75 * u0) + (0.25 * cur)) + (k.qdt * a);
+                    else st = ((u0 / 3.0) + (k.two3 * cur)) + (k.tdt * a);
+                }
+                if (last) s_R[e] = st;
+                else put(e, st);
+            }
+        }
+        if (bad && status) atomicOr(status, MGP_STATUS_NONPOSITIVE_DEPTH);
+    }
+};
+
+template <int K, bool ROE>
+__global__ void __launch_bounds__(256) sys_kernel(const mgp_sweep_args a, const Consts k) {
+    extern __shared__ double smem[];
+    SysField<K, ROE> f;
+    const int nx = (int)a.phi.nx;
+    f.nx = nx;
+    f.pitch = nx + 2 * K;
+    f.s_u = smem;
+    f.s_u0 = f.s_u + 2 * f.pitch;
+    f.s_L = f.s_u0 + 2 * nx;
+    f.s_R = f.s_L + 2 * nx;
+    double *s_sum = f.s_R + 2 * nx;            // [3 * 32]
+    double *s_psum = s_sum + 3 * 32;           // [3]
+    f.s_red = reinterpret_cast<unsigned long long *>(s_psum + 3);
+    f.status = a.status;
+    f.bad = false;
+    sweep_body<SysField<K, ROE>, 1>(a, k, f, 2 * nx, 0, 0, s_sum, s_psum, 2 * nx);
 }
 
 __global__ void __launch_bounds__(1024, 1)
@@ -964,6 +1228,7 @@ Consts make_consts(const mgp_phi &p) {
     k.twodx_pow2 = pow2_normal(k.twodx);
     k.lf_order = p.lf_order;
     k.m_eff = p.m_eff;
+    k.gravity = p.gravity;
     return k;
 }
 
@@ -1167,7 +1432,41 @@ int launch_lf(const mgp_sweep_args &a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
+template <int K, bool ROE>
+int launch_sys_t(const mgp_sweep_args &a, cudaStream_t st) {
+    const int64_t nx = a.phi.nx;
+    int nt = (int)((nx + 31) / 32 * 32);
+    if (nt > 256) nt = 256;
+    const size_t sm = sizeof(double) * (size_t)(2 * (nx + 2 * K) + 6 * nx + 3 * 32 + 3) +
+                      sizeof(unsigned long long) * 32;
+    auto kern = sys_kernel<K, ROE>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024) != cudaSuccess)
+            return MGP_ECUDA;
+        attr_set = true;
+    }
+    int64_t grid = a.n_chunks;
+    if (grid > (int64_t)1 << 30) grid = (int64_t)1 << 30;
+    kern<<<(unsigned)grid, nt, sm, st>>>(a, make_consts(a.phi));
+    ++g_launches;
+    return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
+}
+
+template <bool ROE>
+int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
+    switch (a.phi.weno_k) {
+        case 0: return launch_sys_t<0, ROE>(a, st);
+        case 1: return launch_sys_t<1, ROE>(a, st);
+        case 2: return launch_sys_t<2, ROE>(a, st);
+        case 3: return launch_sys_t<3, ROE>(a, st);
+    }
+    return MGP_EINVAL;
+}
+
 int64_t max_nx_for(int k, int model) {
+    if (model == MGP_MODEL_SHALLOW_WATER) return kMaxSysNx;
     return (k == 2 && model == MGP_MODEL_BURGERS) ? 16 * kMaxNx : kMaxNx;
 }
 
@@ -1175,9 +1474,14 @@ int validate(const mgp_sweep_args *a) {
     if (!a) return MGP_EINVAL;
     const mgp_phi &p = a->phi;
     if (p.repeats < 1) return MGP_EINVAL;
-    if (p.scheme == MGP_SCHEME_RK_WENO_ROE &&
-        (p.model != MGP_MODEL_BURGERS || p.nx > kMaxNx))
+    if (p.model == MGP_MODEL_SHALLOW_WATER) {
+        if (p.scheme != MGP_SCHEME_RK_WENO && p.scheme != MGP_SCHEME_RK_WENO_ROE)
+            return MGP_EINVAL;
+        if (!(p.gravity > 0.0)) return MGP_EINVAL;   // models.py:139-143
+    } else if (p.scheme == MGP_SCHEME_RK_WENO_ROE &&
+               (p.model != MGP_MODEL_BURGERS || p.nx > kMaxNx)) {
         return MGP_EINVAL;
+    }
     if (p.scheme != MGP_SCHEME_RK_WENO && p.scheme != MGP_SCHEME_RK_WENO_ROE) {
         if (p.scheme != MGP_SCHEME_LF_ONESTEP && p.scheme != MGP_SCHEME_LF_MATCHED)
             return MGP_EINVAL;
@@ -1196,12 +1500,15 @@ int validate(const mgp_sweep_args *a) {
         if (a->tail == MGP_TAIL_RESID && (!a->aux || !a->partials)) return MGP_EINVAL;
         return MGP_OK;
     }
-    if (p.model != MGP_MODEL_BURGERS && p.model != MGP_MODEL_ADVECTION) return MGP_EINVAL;
+    if (p.model != MGP_MODEL_BURGERS && p.model != MGP_MODEL_ADVECTION &&
+        p.model != MGP_MODEL_SHALLOW_WATER)
+        return MGP_EINVAL;
     if (p.weno_k < 0 || p.weno_k > 3) return MGP_EINVAL;
     if (p.rk_order < 0 || p.rk_order > 3) return MGP_EINVAL;
     if (p.regime != MGP_SUM_SEQ && p.regime != MGP_SUM_LANE2) return MGP_EINVAL;
     if (p.nx < 2 * p.weno_k + 1 || p.nx > max_nx_for(p.weno_k, p.model)) return MGP_EINVAL;
-    if (p.nx > kMaxNx && p.nx % (((p.nx + kMaxNx - 1) / kMaxNx + 0)) != 0) {
+    if (p.model != MGP_MODEL_SHALLOW_WATER && p.nx > kMaxNx &&
+        p.nx % (((p.nx + kMaxNx - 1) / kMaxNx + 0)) != 0) {
         int cs = 2;
         while (p.nx / cs > kMaxNx || p.nx % cs) {
             cs *= 2;
@@ -1240,6 +1547,9 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (rc != MGP_OK) return rc;
     if (args->n_chunks == 0) return MGP_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (args->phi.model == MGP_MODEL_SHALLOW_WATER)
+        return args->phi.scheme == MGP_SCHEME_RK_WENO_ROE ? launch_sys<true>(*args, st)
+                                                          : launch_sys<false>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_RK_WENO_ROE) return launch_m<kModelBurgersRoe>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
@@ -1257,7 +1567,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
 
 int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
-int32_t mgp_abi_version(void) { return 1; }
+int32_t mgp_abi_version(void) { return 2; }
 
 int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
     if (k < 0 || k > 3 || !cw16 || !d4 || !sm64) return MGP_EINVAL;
@@ -1292,7 +1602,7 @@ int32_t mgp_sweep_args_layout(int64_t *out, int32_t n) {
         MGP_OFF(tg_s), MGP_OFF(tail_out), MGP_OFF(to_s), MGP_OFF(tail_out2),
         MGP_OFF(to2_s), MGP_OFF(aux), MGP_OFF(aux_s), MGP_OFF(aux2), MGP_OFF(aux2_s),
         MGP_OFF(ref), MGP_OFF(ref_cs), MGP_OFF(ref_ss), MGP_OFF(ref_last_next),
-        MGP_OFF(count_nonfinite), MGP_OFF(partials)};
+        MGP_OFF(count_nonfinite), MGP_OFF(partials), MGP_OFF(status)};
 #undef MGP_OFF
     const int32_t total = (int32_t)(sizeof(v) / sizeof(v[0]));
     int32_t i = 0;

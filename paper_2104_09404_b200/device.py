@@ -12,8 +12,9 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (G_NONE, MgpPhi, MgpSweepArgs, SUM_LANE2, SUM_SEQ,
-                   TAIL_NONE)
+from ._lib import (G_NONE, MODEL_SHALLOW_WATER, MgpPhi, MgpSweepArgs,
+                   STATUS_NONPOSITIVE_DEPTH, SUM_LANE2, SUM_SEQ, TAIL_NONE)
+from .errors import PhysicalStateError
 
 DTYPE = torch.float64
 
@@ -67,6 +68,47 @@ def regime_for_batch(n_fields: int) -> int:
     return SUM_SEQ if n_fields >= 2 else SUM_LANE2
 
 
+# Per-device status word (int32) the shallow-water kernels OR
+# MGP_STATUS_* bits into where the reference raises PhysicalStateError
+# (models.py:147-153).  Sweeps are asynchronous, so callers check it at
+# their synchronisation points (check_status).
+_status_words = {}
+
+
+def status_word() -> torch.Tensor:
+    d = device()
+    w = _status_words.get(d)
+    if w is None:
+        w = torch.zeros(1, dtype=torch.int32, device=d)
+        _status_words[d] = w
+    return w
+
+
+def take_status() -> int:
+    """Read and clear the status word (synchronises with its stream)."""
+    w = _status_words.get(device())
+    if w is None:
+        return 0
+    v = int(w.item())
+    if v:
+        w.zero_()
+    return v
+
+
+def raise_for_status(v: int) -> None:
+    if v & STATUS_NONPOSITIVE_DEPTH:
+        raise PhysicalStateError("non-positive depth met by the shallow-water "
+                                 "propagator (models.py:147-153)")
+    if v:
+        raise PhysicalStateError(f"propagator status {v}")
+
+
+def check_status() -> None:
+    """Raise PhysicalStateError if a sweep since the last check met a
+    state the reference rejects."""
+    raise_for_status(take_status())
+
+
 def ptr(t) -> int | None:
     if t is None:
         return None
@@ -83,7 +125,10 @@ def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
           tg_s: int = 0, tail_out=None, to_s: int = 0, tail_out2=None,
           to2_s: int = 0, aux=None, aux_s: int = 0, aux2=None, aux2_s: int = 0,
           ref=None, ref_cs: int = 0, ref_ss: int = 0, ref_last_next: int = 0,
-          count_nonfinite: int = 0, partials=None, what: str = "mgp_sweep"):
+          count_nonfinite: int = 0, partials=None, status=None,
+          what: str = "mgp_sweep"):
+    if status is None and phi.model == MODEL_SHALLOW_WATER:
+        status = status_word()
     if _emulator is not None:
         kw = dict(locals())
         kw.pop("phi")
@@ -106,6 +151,7 @@ def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
     a.ref_last_next = int(ref_last_next)
     a.count_nonfinite = int(count_nonfinite)
     a.partials = ptr(partials)
+    a.status = ptr(status)
     rc = _lib.load().mgp_sweep(ctypes.byref(a), ctypes.c_void_p(stream_handle()))
     _lib.check(rc, what)
 

@@ -76,11 +76,14 @@ class DistMgritHierarchy:
         self.r = dist.get_rank(group)
         self.device = dev.device()
         u0 = dev.to_device(initial_state)
-        if u0.dim() != 2 or u0.shape[0] != 1:
-            raise DimensionError(f"initial state must be (1, N), got {tuple(u0.shape)}")
-        self.nx = nx = u0.shape[1]
-        self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
-        self._u0 = u0[0].contiguous()
+        Dc = getattr(steppers[0], "n_components", 1) if len(steppers) else 1
+        if u0.dim() != 2 or u0.shape[0] != Dc:
+            raise DimensionError(f"initial state must be ({Dc}, N), got {tuple(u0.shape)}")
+        self.n_components = Dc
+        self.n_cells = u0.shape[1]
+        self.nx = nx = Dc * self.n_cells          # row length
+        self.steppers = [_check_stepper(s, l, self.n_cells, Dc) for l, s in enumerate(steppers)]
+        self._u0 = u0.reshape(-1).contiguous()
         self.n = [time_grid.n_steps // m ** l for l in range(L)]
         self.c = [self.n[l] // m for l in range(L - 1)]
         self.D, self.nloc = partition(time_grid.n_steps, m, L, self.R)
@@ -434,13 +437,13 @@ class DistMgritHierarchy:
         out = torch.empty(self.n[0] + 1, nx, dtype=dev.DTYPE, device=self.device)
         for q, p in enumerate(parts):
             out[q * n0 * m: (q + 1) * n0 * m + 1].copy_(p)
-        return out.view(-1, 1, nx)
+        return out.view(-1, self.n_components, self.n_cells)
 
     def level_values(self, l: int) -> torch.Tensor | None:
         """Level l >= 1 u array assembled on rank 0 (tests)."""
         m = self.options.m
         if l >= self.D:
-            return self._u[l].view(-1, 1, self.nx) if self.r == 0 else None
+            return self._u[l].view(-1, self.n_components, self.n_cells) if self.r == 0 else None
         parts = self._gather_rows(self._u[l])
         if self.r != 0:
             return None
@@ -448,7 +451,7 @@ class DistMgritHierarchy:
         out = torch.empty(self.n[l] + 1, self.nx, dtype=dev.DTYPE, device=self.device)
         for q, p in enumerate(parts):
             out[q * k: (q + 1) * k + 1].copy_(p)
-        return out.view(-1, 1, self.nx)
+        return out.view(-1, self.n_components, self.n_cells)
 
     def load_c_points(self, local_c_points) -> None:
         """Set this rank's finest C-points (n0 + 1 rows incl. halo)."""
@@ -481,11 +484,19 @@ def mgrit_solve_distributed(steppers, initial_state, time_grid, space_grid,
     def error(mon):
         return math.nan if ref is None else math.sqrt(mon.error_sq) / ref_norm
 
-    mon = h.monitor(ref)
+    def watch(mon):
+        # shallow water: every rank raises PhysicalStateError together
+        if h.n_components > 1:
+            flag = torch.tensor([dev.take_status()], dtype=torch.int64, device=h.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+            dev.raise_for_status(int(flag.item()))
+        return mon
+
+    mon = watch(h.monitor(ref))
     errors[0], residuals[0] = error(mon), mon.residual
     for it in range(1, rows):
         h.run_cycle()
-        mon = h.monitor(ref)
+        mon = watch(h.monitor(ref))
         err = error(mon)
         if mon.nonfinite != 0 or (np.isfinite(err) and err > options.divergence_threshold):
             diverged, at = True, it

@@ -5,8 +5,9 @@ Mirrors reference ``pkg/src/mgritlab/flux.py``: ``WenoConfig`` /
 constructor checks (:129-145) and ``rhs`` (:159-161).  The operator only
 holds parameters; ``rhs(field)`` runs on the GPU (``mgp_sweep`` with
 rk_order 0).  The Roe flux with the Harten-Hyman entropy fix
-(flux.py:91-126) is supported for Burgers; systems are rejected with
-ConfigError; there is no CPU fallback.
+(flux.py:91-126) is supported for Burgers and shallow water; the shallow-water
+system uses characteristic WENO (weno.py:222-233) on (..., 2, N) states.
+There is no CPU fallback.
 """
 from __future__ import annotations
 
@@ -67,12 +68,16 @@ class SemiDiscreteOperator:
         if space_grid.n_cells < 2 * config.weno.degree + 1:
             raise ConfigError(f"{space_grid.n_cells} cells cannot support order "
                               f"{config.weno.order} reconstruction")
-        if config.kind == "roe" and getattr(model, "kind", "") != "burgers":
-            raise ConfigError("the B200 path implements the Roe flux for Burgers only "
-                              "(systems are out of scope)")
-        if getattr(model, "n_components", None) != 1 or not hasattr(model, "abi_model"):
+        kind = getattr(model, "kind", "")
+        if config.kind == "roe" and kind not in ("burgers", "shallow-water"):
+            raise ConfigError(f"the B200 path implements the Roe flux for Burgers and "
+                              f"shallow water, not '{kind}'")
+        if not hasattr(model, "abi_model"):
             raise ConfigError(f"model '{getattr(model, 'kind', model)}' is not a "
-                              "scalar model of the B200 path")
+                              "model of the B200 path")
+        if space_grid.n_cells > dev._lib.max_nx_static(config.weno.degree, model.abi_model):
+            raise ConfigError(f"{space_grid.n_cells} cells exceed the {kind} kernel's "
+                              f"limit")
         self.model = model
         self.space_grid = space_grid
         self.config = config
@@ -84,7 +89,11 @@ class SemiDiscreteOperator:
                       float(dt), float(self.space_grid.dx),
                       float(self.config.weno.epsilon), float(self.model.speed),
                       SCHEME_RK_WENO_ROE if self.config.kind == "roe" else SCHEME_RK_WENO,
-                      0, 0, 1)
+                      0, 0, 1, float(getattr(self.model, "gravity", 0.0)))
+
+    @property
+    def n_components(self) -> int:
+        return self.model.n_components
 
     def rhs(self, field_):
         """SemiDiscreteOperator.rhs (flux.py:159-161) on the GPU.  Returns the
@@ -93,26 +102,33 @@ class SemiDiscreteOperator:
 
 
 def apply_phi(op: SemiDiscreteOperator, dt: float, rk_order: int, u):
-    """Phi (or the rhs for rk_order 0) on every (1, N) field of u."""
+    """Phi (or the rhs for rk_order 0) on every (D, N) field of u."""
     return apply_phi_struct(lambda regime: op.phi_struct(dt=dt, rk_order=rk_order,
                                                          regime=regime),
-                            op.space_grid.n_cells, u)
+                            op.space_grid.n_cells, u, op.n_components)
 
 
-def apply_phi_struct(make_phi, nx: int, u):
-    """Run the propagator built by ``make_phi(regime)`` on every (1, N) field
-    of u (regime = NumPy's summation order for that batch size)."""
+def apply_phi_struct(make_phi, nx: int, u, n_components: int = 1):
+    """Run the propagator built by ``make_phi(regime)`` on every (D, N) field
+    of u (regime = NumPy's summation order for that batch size).  Shallow
+    water: synchronises and raises PhysicalStateError where the reference
+    would (models.py:147-153)."""
     is_tensor = torch.is_tensor(u)
     x = dev.to_device(u)
-    if x.dim() < 2 or x.shape[-1] != nx or x.shape[-2] != 1:
-        raise DimensionError(f"expected (..., 1, {nx}) states, got {tuple(x.shape)}")
-    batch = x.numel() // nx
+    D = int(n_components)
+    if x.dim() < 2 or x.shape[-1] != nx or x.shape[-2] != D:
+        raise DimensionError(f"expected (..., {D}, {nx}) states, got {tuple(x.shape)}")
+    row = D * nx
+    batch = x.numel() // row
     out = torch.empty_like(x)
     if batch:
         regime = dev.regime_for_batch(batch)
-        dev.sweep(make_phi(regime), n_chunks=batch, start=x, start_stride=nx,
-                  tail=TAIL_PHI, tail_regime=regime, tail_out=out, to_s=nx,
+        phi = make_phi(regime)
+        dev.sweep(phi, n_chunks=batch, start=x, start_stride=row,
+                  tail=TAIL_PHI, tail_regime=regime, tail_out=out, to_s=row,
                   what="advance")
+        if D > 1:
+            dev.check_status()
     if is_tensor:
         return out
     return out.cpu().numpy()

@@ -110,6 +110,29 @@ def sine_ic(space_grid: SpatialGrid) -> np.ndarray:
     return discretise_ic(lambda x: np.sin(2.0 * np.pi * x), space_grid)
 
 
+def _sin(x, length):
+    return np.sin(2.0 * np.pi * x / length)
+
+
+# reference harness.py:29-75: the named initial conditions of the configs
+NAMED_ICS = {
+    "sin-stationary": lambda x, L: _sin(x, L)[None, :],
+    "sin-moving": lambda x, L: (0.5 * (1.0 + _sin(x, L)))[None, :],
+    "burgers-43": lambda x, L: ((4.0 / 3.0) * _sin(x, L))[None, :],
+    "sw-scaled": lambda x, L: np.stack([(1.0 + 0.5 * _sin(x, L)) / 11.0,
+                                        np.zeros_like(x)]),
+}
+
+
+def named_ic(name: str, space_grid: SpatialGrid) -> np.ndarray:
+    """A named initial condition of the reference configs at cell midpoints,
+    shape (D, N)."""
+    if name not in NAMED_ICS:
+        raise ConfigError(f"unknown initial condition '{name}', expected one of "
+                          f"{sorted(NAMED_ICS)}")
+    return NAMED_ICS[name](space_grid.cell_centers(), space_grid.length)
+
+
 def cfl_horizon(n_steps: int, cfl: float, dx: float, max_speed: float) -> float:
     return n_steps * (cfl * dx / max_speed)
 
@@ -136,7 +159,7 @@ class Problem:
     n_x: int = 512
     n_t: int = 4096
     cfl: float = 0.4
-    ic: str = "fourier"        # "fourier" | "sine"
+    ic: str = "fourier"        # "fourier" | "sine" | a NAMED_ICS key
     n_modes: int = 4
     decay: bool = False
     seed: int = 1234
@@ -152,6 +175,9 @@ class Problem:
     epsilon: float = DEFAULT_EPSILON
     length: float = 1.0
     coarse: str = "rediscretize"
+    flux: str = "lf"
+    gravity: float = 9.81
+    horizon: float | None = None   # fixed T (reference configs) instead of the CFL rule
 
     def scaled(self, **kw) -> "Problem":
         return replace(self, **kw)
@@ -163,12 +189,16 @@ class Problem:
         sg = self.space_grid()
         if self.ic == "sine":
             return sine_ic(sg)
+        if self.ic in NAMED_ICS:
+            return named_ic(self.ic, sg)
         return fourier_ic(sg, self.n_modes, self.seed, self.decay)
 
     def model_obj(self):
-        return make_model(self.model, speed=self.speed)
+        return make_model(self.model, speed=self.speed, gravity=self.gravity)
 
     def time_grid(self, u0: np.ndarray | None = None) -> TemporalGrid:
+        if self.horizon is not None:
+            return TemporalGrid(self.horizon, self.n_t)
         u0 = self.initial_state() if u0 is None else u0
         sg = self.space_grid()
         speed = abs(self.speed) if self.model == "advection" else float(np.max(np.abs(u0)))
@@ -179,7 +209,8 @@ class Problem:
         return build_steppers(self.model_obj(), self.space_grid(), tg,
                               n_levels=self.n_levels, m=self.m,
                               weno_order=self.weno_order, stepper=self.stepper,
-                              epsilon=self.epsilon, coarse=self.coarse)
+                              epsilon=self.epsilon, coarse=self.coarse,
+                              flux=self.flux)
 
     def options(self):
         from .mgrit import MgritOptions

@@ -109,7 +109,7 @@ class Monitor:
 
 class MgritLevel:
     """Per-level view (mgrit.py:82-89).  For l >= 1, ``u`` / ``g`` are the
-    device arrays (n_intervals + 1, 1, N).  For l = 0, ``u`` materialises the
+    device arrays (n_intervals + 1, D, N).  For l = 0, ``u`` materialises the
     full trajectory on demand (a device snapshot) and ``g`` is the implicit
     finest right-hand side (initial state at node 0, zero elsewhere)."""
 
@@ -124,22 +124,22 @@ class MgritLevel:
     def u(self):
         if self.index == 0:
             return self._h.fine_values()
-        return self._h._u[self.index].view(self.n_intervals + 1, 1, -1)
+        return self._h._u[self.index].view(self.n_intervals + 1, self._h.n_components, -1)
 
     @property
     def g(self):
+        h = self._h
         if self.index == 0:
-            g = torch.zeros(self.n_intervals + 1, 1, self._h.nx, dtype=dev.DTYPE,
-                            device=self._h.device)
-            g[0, 0] = self._h._u0
-            return g
-        return self._h._g[self.index].view(self.n_intervals + 1, 1, -1)
+            g = torch.zeros(self.n_intervals + 1, h.nx, dtype=dev.DTYPE, device=h.device)
+            g[0] = h._u0
+            return g.view(self.n_intervals + 1, h.n_components, -1)
+        return h._g[self.index].view(self.n_intervals + 1, h.n_components, -1)
 
 
 _PROPAGATORS = (RungeKuttaStepper, _LFStepper, ComposedStepper)
 
 
-def _check_stepper(s, l: int, nx: int):
+def _check_stepper(s, l: int, nx: int, n_components: int):
     if not isinstance(s, _PROPAGATORS):
         raise ConfigError(
             f"level {l}: the B200 hierarchy runs this package's propagators "
@@ -147,6 +147,9 @@ def _check_stepper(s, l: int, nx: int):
             f"got {type(s).__name__}")
     if s.nx != nx:
         raise DimensionError(f"level {l}: stepper mesh has {s.nx} cells, state has {nx}")
+    if s.n_components != n_components:
+        raise DimensionError(f"level {l}: stepper works on {s.n_components} components, "
+                             f"state has {n_components}")
     return s
 
 
@@ -154,7 +157,7 @@ def _nx_limit(s) -> int:
     inner = s.inner if isinstance(s, ComposedStepper) else s
     if isinstance(inner, RungeKuttaStepper):
         op = inner.operator
-        if op.config.kind == "roe":
+        if op.config.kind == "roe" and op.model.n_components == 1:
             return 4096
         return dev._lib.max_nx(op.config.weno.degree, op.model.abi_model)
     return 2048   # one-step LF family (kMaxLfNx)
@@ -176,17 +179,21 @@ class MgritHierarchy:
         self.space_grid = space_grid
         self.device = dev.device()
         u0 = dev.to_device(initial_state)
-        if u0.dim() != 2 or u0.shape[0] != 1:
-            raise DimensionError(f"initial state must be (1, N), got {tuple(u0.shape)}")
-        self.nx = nx = u0.shape[1]
-        self.steppers = [_check_stepper(s, l, nx) for l, s in enumerate(steppers)]
+        D = getattr(steppers[0], "n_components", 1) if len(steppers) else 1
+        if u0.dim() != 2 or u0.shape[0] != D:
+            raise DimensionError(f"initial state must be ({D}, N), got {tuple(u0.shape)}")
+        self.n_components = D
+        self.n_cells = cells = u0.shape[1]
+        # row length: the D components of one state, component-major
+        self.nx = nx = D * cells
+        self.steppers = [_check_stepper(s, l, cells, D) for l, s in enumerate(steppers)]
         if not dev.emulated():
             for l, s in enumerate(self.steppers):
                 lim = _nx_limit(s)
-                if nx > lim:
-                    raise ConfigError(f"level {l}: N_x = {nx} exceeds the field limit "
+                if cells > lim:
+                    raise ConfigError(f"level {l}: N_x = {cells} exceeds the field limit "
                                       f"{lim} of this build for {type(s).__name__}")
-        self._u0 = u0[0].contiguous()
+        self._u0 = u0.reshape(-1).contiguous()
         self.n = [time_grid.n_steps // m ** l for l in range(L)]
         self.levels = [MgritLevel(self, l, time_grid.dt * m ** l, self.n[l], steppers[l])
                        for l in range(L)]
@@ -421,7 +428,7 @@ class MgritHierarchy:
         return self.monitor().residual
 
     def fine_values(self, out: torch.Tensor | None = None) -> torch.Tensor:
-        """The finest-level trajectory (N_t + 1, 1, N) as a device tensor,
+        """The finest-level trajectory (N_t + 1, D, N) as a device tensor,
         F-points recomputed from the C-points they derive from (written into
         ``out`` when given)."""
         m, nx, nt = self.options.m, self.nx, self.n[0]
@@ -439,7 +446,7 @@ class MgritHierarchy:
                       start=self._c[self._fsrc], start_stride=nx, n_steps=m - 1,
                       g_mode=G_ZERO, store=out[1], st_cs=m * nx, st_ss=nx,
                       what="fine_values")
-        return out.view(nt + 1, 1, nx)
+        return out.view(nt + 1, self.n_components, self.n_cells)
 
     def load_c_points(self, c_points) -> None:
         """Set the finest-level C-points (N_t/m + 1 rows, host or device) and
@@ -544,8 +551,8 @@ class MgritHierarchy:
         self._pristine = False
 
     def c_points(self) -> torch.Tensor:
-        """Current finest-level C-points (N_t/m + 1, 1, N), device view."""
-        return self._c[self._cur].view(-1, 1, self.nx)
+        """Current finest-level C-points (N_t/m + 1, D, N), device view."""
+        return self._c[self._cur].view(-1, self.n_components, self.n_cells)
 
 
 def _ref_norm_sq(reference: torch.Tensor, nx: int, stepper) -> float:
@@ -571,7 +578,7 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     when a reference is supplied) is recorded, not raised, and that row plus
     all later rows stay NaN.
 
-    reference: serial trajectory (N_t + 1, 1, N), host array or CUDA tensor.
+    reference: serial trajectory (N_t + 1, D, N), host array or CUDA tensor.
     Returns (Trajectory, ConvergenceRecord); the trajectory values are a host
     array (``return_trajectory=False`` skips materialising it, e.g. for
     problems whose full trajectory does not fit in memory).  residual_tol
@@ -609,14 +616,21 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     errors = np.full(n_rows, np.nan)
     residuals = np.full(n_rows, np.nan)
     diverged, diverged_at, converged_at = False, None, None
-    mon = h.monitor(ref)
+    checked = h.n_components > 1    # shallow water: PhysicalStateError
+
+    def watch(mon):
+        if checked:
+            dev.check_status()
+        return mon
+
+    mon = watch(h.monitor(ref))
     errors[0] = error(mon)
     residuals[0] = mon.residual
     for it in range(1, n_rows):
         if residual_tol is not None and converged_at is not None:
             break
         h.run_cycle()
-        mon = h.monitor(ref)
+        mon = watch(h.monitor(ref))
         err = error(mon)
         finite = mon.nonfinite == 0
         if not finite or (np.isfinite(err) and err > options.divergence_threshold):

@@ -4,9 +4,12 @@
 (0.5 u) u, eigenvalue u, max speed |u|).  ``Advection`` is the linear model
 BASELINE.json config 1 needs (u_t + a u_x = 0, flux a u, |lambda| = |a|);
 the reference rejects "advection" (tests/test_models.py:197-198), so it is a
-new ``ConservationModel`` subclass with the same shape contract.  The
-systems (shallow water, Euler, models.py:136-308) are outside the GPU path's
-scope: ``make_model`` raises ConfigError for them.
+new ``ConservationModel`` subclass with the same shape contract.
+``ShallowWater`` mirrors models.py:136-211 (state (h, hu), gravity g); its
+propagator is the characteristic-WENO system kernel.  The Euler system
+(models.py:214-308) is out of scope: its characteristic projection in the
+reference goes through LAPACK ``np.linalg.inv`` per cell, whose rounding a
+kernel cannot reproduce bit for bit, so ``make_model`` raises ConfigError.
 
 These host methods are the reference's NumPy semantics for callers and
 tests; the device kernels implement the same formulas (csrc/mgrit_phi.cu).
@@ -15,10 +18,12 @@ from __future__ import annotations
 
 import numpy as np
 
-from .errors import ConfigError, DimensionError
+from .errors import ConfigError, DimensionError, PhysicalStateError
 
-MODEL_BURGERS = 0    # MGP_MODEL_BURGERS
-MODEL_ADVECTION = 1  # MGP_MODEL_ADVECTION
+MODEL_BURGERS = 0         # MGP_MODEL_BURGERS
+MODEL_ADVECTION = 1       # MGP_MODEL_ADVECTION
+MODEL_SHALLOW_WATER = 2   # MGP_MODEL_SHALLOW_WATER
+DEFAULT_GRAVITY = 9.81    # models.py:21
 
 
 class ConservationModel:
@@ -91,18 +96,61 @@ class Advection(ConservationModel):
         return np.full(u[..., 0, :].shape, abs(self.speed))
 
 
-_MODEL_KINDS = ("burgers", "advection")
-_OUT_OF_SCOPE = ("shallow-water", "euler")
+class ShallowWater(ConservationModel):
+    """Depth/momentum system (h, hu) with gravity wave speeds u -+ sqrt(g h)
+    (models.py:136-183)."""
+
+    kind = "shallow-water"
+    n_components = 2
+    abi_model = MODEL_SHALLOW_WATER
+    speed = 0.0
+
+    def __init__(self, gravity: float = DEFAULT_GRAVITY):
+        if not gravity > 0.0:
+            raise PhysicalStateError(f"gravity must be positive, got {gravity}")
+        self.gravity = float(gravity)
+
+    def _depth_velocity(self, u):
+        h = u[..., 0, :]
+        bad = h <= 0.0
+        if np.any(bad):
+            raise PhysicalStateError(
+                f"non-positive depth in cell {int(np.argmax(bad.reshape(-1)))}")
+        return h, u[..., 1, :] / h
+
+    def flux(self, u):
+        self._check_shape(u)
+        h, vel = self._depth_velocity(u)
+        return np.stack([u[..., 1, :], h * vel * vel + 0.5 * self.gravity * h * h],
+                        axis=-2)
+
+    def eigenvalues(self, u):
+        self._check_shape(u)
+        h, vel = self._depth_velocity(u)
+        c = np.sqrt(self.gravity * h)
+        return np.stack([vel - c, vel + c], axis=-1)
+
+    def max_abs_speed(self, u):
+        self._check_shape(u)
+        h, vel = self._depth_velocity(u)
+        return np.abs(vel) + np.sqrt(self.gravity * h)
 
 
-def make_model(kind: str, *, speed: float = 1.0, **_unused) -> ConservationModel:
+_MODEL_KINDS = ("burgers", "advection", "shallow-water")
+_OUT_OF_SCOPE = ("euler",)
+
+
+def make_model(kind: str, *, speed: float = 1.0, gravity: float = DEFAULT_GRAVITY,
+               **_unused) -> ConservationModel:
     """Build a model by name (models.py:318-328 plus "advection")."""
     if kind == "burgers":
         return Burgers()
     if kind == "advection":
         return Advection(speed)
+    if kind == "shallow-water":
+        return ShallowWater(gravity)
     if kind in _OUT_OF_SCOPE:
         raise ConfigError(
-            f"model '{kind}' is a system; the B200 path implements the scalar "
-            f"models {_MODEL_KINDS} only")
+            f"model '{kind}' is outside the B200 path (its characteristic "
+            f"projection uses LAPACK inverses); supported: {_MODEL_KINDS}")
     raise ConfigError(f"unknown model '{kind}', expected one of {sorted(_MODEL_KINDS)}")

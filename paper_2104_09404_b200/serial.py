@@ -43,16 +43,22 @@ def discretise_ic(ic, space_grid: SpatialGrid) -> np.ndarray:
 
 
 def march(stepper, initial_state, n_steps: int) -> torch.Tensor:
-    """Device trajectory (n_steps + 1, 1, N): u[i] = Phi(u[i-1])."""
+    """Device trajectory (n_steps + 1, D, N): u[i] = Phi(u[i-1])."""
+    D = getattr(stepper, "n_components", 1)
     u0 = dev.to_device(initial_state).reshape(-1)
     nx = u0.numel()
+    if nx != D * stepper.nx:
+        raise DimensionError(f"initial state has {nx} values, the stepper works on "
+                             f"({D}, {stepper.nx}) states")
     out = torch.empty(n_steps + 1, nx, dtype=dev.DTYPE, device=u0.device)
     out[0].copy_(u0)
     if n_steps:
         dev.sweep(stepper.phi_struct(dev.regime_for_batch(1)), n_chunks=1,
                   start=out, start_stride=0, n_steps=n_steps, g_mode=G_NONE,
                   store=out[1], st_ss=nx, what="solve_serial")
-    return out.view(n_steps + 1, 1, nx)
+        if D > 1:
+            dev.check_status()
+    return out.view(n_steps + 1, D, nx // D)
 
 
 def solve_serial(stepper, initial_state, time_grid: TemporalGrid,
@@ -65,6 +71,14 @@ def solve_serial(stepper, initial_state, time_grid: TemporalGrid,
     if model is not None:
         if getattr(model, "kind", "") == "advection":
             max_speed = abs(model.speed)
+        elif getattr(model, "kind", "") == "shallow-water":
+            # serial.py:47-54: running max over nodes of max |u| + sqrt(g h)
+            # (Python max ignores NaN nodes after the first)
+            h, hu = values[:, 0, :], values[:, 1, :]
+            per_node = ((hu / h).abs() + torch.sqrt(model.gravity * h)).amax(dim=1)
+            per_node = torch.where(torch.isnan(per_node), torch.zeros_like(per_node),
+                                   per_node)
+            max_speed = float(per_node.max().item())
         else:
             per_node = values.abs().amax(dim=(1, 2))
             per_node = torch.where(torch.isnan(per_node), torch.zeros_like(per_node),

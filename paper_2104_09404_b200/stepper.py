@@ -50,7 +50,7 @@ class RungeKuttaStepper:
         self.order = order
 
     def advance(self, u):
-        """One step on every (1, N) field of u (stepper.py:81-82).  NumPy in
+        """One step on every (D, N) field of u (stepper.py:81-82).  NumPy in
         -> NumPy out; CUDA tensor in -> CUDA tensor out."""
         return apply_phi(self.operator, self.dt, self.order, u)
 
@@ -60,6 +60,10 @@ class RungeKuttaStepper:
     @property
     def nx(self) -> int:
         return self.operator.space_grid.n_cells
+
+    @property
+    def n_components(self) -> int:
+        return self.operator.n_components
 
 
 def neighbor_average(u):
@@ -84,6 +88,7 @@ class _LFStepper:
     scheme = SCHEME_LF_ONESTEP
     lf_order = 0
     m_effective = 1
+    n_components = 1
 
     def _formula_dt(self) -> float:
         return self.dt
@@ -153,6 +158,7 @@ class ComposedStepper:
         self.repeats = repeats
         self.dt = inner.dt * repeats
         self.nx = inner.nx
+        self.n_components = getattr(inner, "n_components", 1)
 
     @property
     def operator(self):
@@ -164,7 +170,7 @@ class ComposedStepper:
         return p
 
     def advance(self, u):
-        return apply_phi_struct(self.phi_struct, self.nx, u)
+        return apply_phi_struct(self.phi_struct, self.nx, u, self.n_components)
 
 
 @dataclass(frozen=True)

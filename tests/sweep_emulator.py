@@ -10,7 +10,7 @@ import torch
 
 import oracle
 
-_MODEL = {0: "burgers", 1: "advection"}
+_MODEL = {0: "burgers", 1: "advection", 2: "shallow-water"}
 
 
 def _rows(t, stride, n, nx, off=0):
@@ -22,7 +22,17 @@ def _params(phi, regime):
     return oracle.make_params(model=_MODEL[phi.model], k=phi.weno_k, rk_order=phi.rk_order,
                               dt=phi.dt, dx=phi.dx, eps=phi.epsilon, speed=phi.speed,
                               regime=regime, scheme=phi.scheme, lf_order=phi.lf_order,
-                              m_eff=phi.m_eff, repeats=phi.repeats)
+                              m_eff=phi.m_eff, repeats=phi.repeats, gravity=phi.gravity)
+
+
+def _apply(p, x, n, D, nx, status):
+    try:
+        return oracle.phi_apply(p, x.reshape(n, D, nx)).reshape(n, D * nx)
+    except oracle.PhysicalStateOracleError:
+        # the kernel flags the status word and completes the sweep
+        if status is not None:
+            status.view(-1)[0] |= 1
+        return np.full((n, D * nx), np.nan)
 
 
 def _add_g(y, mode, g):
@@ -36,8 +46,10 @@ def _add_g(y, mode, g):
 def emulate_sweep(phi, *, n_chunks, start, start_stride, n_steps, g_mode, g, g_cs, g_ss,
                   store, st_cs, st_ss, tail, tail_regime, tail_g_mode, guess, tail_g, tg_s,
                   tail_out, to_s, tail_out2, to2_s, aux, aux_s, aux2, aux2_s, ref, ref_cs,
-                  ref_ss, ref_last_next, count_nonfinite, partials, what):
-    n, nx = int(n_chunks), int(phi.nx)
+                  ref_ss, ref_last_next, count_nonfinite, partials, status, what):
+    D = 2 if phi.model == 2 else 1
+    n, cells = int(n_chunks), int(phi.nx)
+    nx = D * cells   # row length
     if n == 0:
         return
     with np.errstate(all="ignore"):
@@ -56,14 +68,14 @@ def emulate_sweep(phi, *, n_chunks, start, start_stride, n_steps, g_mode, g, g_c
         account(x, 0)
         p = _params(phi, phi.regime)
         for s in range(1, n_steps + 1):
-            y = oracle.phi_apply(p, x.reshape(n, 1, nx)).reshape(n, nx)
+            y = _apply(p, x, n, D, cells, status)
             gr = _rows(g, g_cs, n, nx, (s - 1) * g_ss).numpy() if g is not None else None
             x = _add_g(y, g_mode, gr)
             if store is not None:
                 _rows(store, st_cs, n, nx, (s - 1) * st_ss).copy_(torch.from_numpy(x))
             account(x, s)
         if tail:
-            y = oracle.phi_apply(_params(phi, tail_regime), x.reshape(n, 1, nx)).reshape(n, nx)
+            y = _apply(_params(phi, tail_regime), x, n, D, cells, status)
             tg = _rows(tail_g, tg_s, n, nx).numpy() if tail_g is not None else None
             if tail == 1:
                 _rows(tail_out, to_s, n, nx).copy_(torch.from_numpy(_add_g(y, tail_g_mode, tg)))

@@ -54,13 +54,20 @@ def test_device_tables_equal_rational_tables(k):
 
 def test_abi_constants():
     lib = _lib.load()
-    assert lib.mgp_abi_version() == 1
+    assert lib.mgp_abi_version() == _lib.ABI_VERSION
     assert lib.mgp_max_nx(2, 0) == 65536 and lib.mgp_max_nx(1, 0) == 4096
+    assert lib.mgp_max_nx(2, 2) == 2048
+    for k in range(4):
+        for model in range(3):
+            assert lib.mgp_max_nx(k, model) == _lib.max_nx_static(k, model)
     assert lib.mgp_launch_count() >= 0
     hdr = open(_lib.HEADER_PATH).read()
     for name, val in [("MGP_SUM_SEQ", _lib.SUM_SEQ), ("MGP_SUM_LANE2", _lib.SUM_LANE2),
                       ("MGP_G_ZERO", _lib.G_ZERO), ("MGP_G_ARRAY", _lib.G_ARRAY),
                       ("MGP_TAIL_PHI", _lib.TAIL_PHI), ("MGP_TAIL_RESTRICT", _lib.TAIL_RESTRICT),
                       ("MGP_TAIL_RESID", _lib.TAIL_RESID),
-                      ("MGP_GUESS_INJECTION", _lib.GUESS_INJECTION)]:
+                      ("MGP_GUESS_INJECTION", _lib.GUESS_INJECTION),
+                      ("MGP_MODEL_SHALLOW_WATER", _lib.MODEL_SHALLOW_WATER),
+                      ("MGP_STATUS_NONPOSITIVE_DEPTH", _lib.STATUS_NONPOSITIVE_DEPTH),
+                      ("MGP_SCHEME_RK_WENO_ROE", _lib.SCHEME_RK_WENO_ROE)]:
         assert re.search(rf"#define {name} {val}\b", hdr), name

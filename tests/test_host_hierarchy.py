@@ -104,3 +104,53 @@ def test_lf_family_hierarchy_matches_oracle():
         ok = np.isfinite(want)
         np.testing.assert_allclose(rec.errors[ok], want[ok], rtol=1e-10)
         assert rec.diverged_at == spec["diverged_at"]
+
+
+def _sw_setup(name):
+    import json, os
+    g = os.path.join(os.path.dirname(__file__), "golden")
+    meta = {m["name"]: m for m in json.load(open(os.path.join(g, "sw_mgrit_cases.json")))}
+    data = np.load(os.path.join(g, "sw_mgrit_cases.npz"))
+    spec = meta[name]
+    sg = P.SpatialGrid(spec["length"], spec["n_x"])
+    tg = P.TemporalGrid(spec["horizon"], spec["n_t"])
+    steppers = P.build_steppers(P.make_model("shallow-water", gravity=spec["gravity"]), sg, tg,
+                                n_levels=spec["n_levels"], m=spec["m"],
+                                weno_order=spec["weno_order"], stepper=spec["stepper"],
+                                flux=spec["flux"])
+    opts = P.MgritOptions(n_levels=spec["n_levels"], m=spec["m"], cycle=spec["cycle"],
+                          relaxation=spec["relaxation"], guess=spec["guess"],
+                          max_iters=spec["max_iters"])
+    return spec, data, sg, tg, steppers, opts
+
+
+@pytest.mark.parametrize("name", ["high_order_shallow_water_lf__3",
+                                  "high_order_shallow_water_roe__1"])
+def test_shallow_water_hierarchy_matches_reference(name):
+    """(2, N) states through the hierarchy bookkeeping (rows of 2 N_x,
+    emulated kernels): the reference config's history and trajectory."""
+    spec, data, sg, tg, steppers, opts = _sw_setup(name)
+    u0 = data[name + "__u0"]
+    assert np.array_equal(u0, P.harness.named_ic("sw-scaled", sg))
+    serial = P.solve_serial(steppers[0], u0, tg, sg, P.make_model("shallow-water"))
+    assert serial.trajectory.values.shape == (spec["n_t"] + 1, 2, spec["n_x"])
+    traj, rec = P.mgrit_solve(steppers, u0, tg, sg, opts, reference=serial.device_values)
+    np.testing.assert_allclose(rec.errors, data[name + "__errors"], rtol=1e-12, atol=0)
+    assert rec.diverged_at == spec["diverged_at"]
+    assert np.array_equal(traj.values, data[name + "__traj"])
+
+
+def test_shallow_water_dry_state_raises():
+    """Non-positive depth: PhysicalStateError like the reference
+    (models.py:147-153), from advance and from mgrit_solve."""
+    spec, data, sg, tg, steppers, opts = _sw_setup("high_order_shallow_water_lf__1")
+    u0 = data["high_order_shallow_water_lf__1__u0"].copy()
+    bad = np.stack([u0, u0])
+    bad[1, 0, 3] = -1e-3
+    with pytest.raises(P.PhysicalStateError):
+        steppers[0].advance(bad)
+    # a good state afterwards is fine (the status word was cleared)
+    steppers[0].advance(u0)
+    u0[0, 7] = 0.0
+    with pytest.raises(P.PhysicalStateError):
+        P.mgrit_solve(steppers, u0, tg, sg, opts)
