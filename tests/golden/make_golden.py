@@ -579,9 +579,47 @@ def sw_mgrit_cases():
         json.dump(meta, f, indent=1)
 
 
+# ---------------------------------------------------------------------------
+# the checked-in experiment configs through the reference harness
+# (harness.py:369-495) -- SURVEY.md 8(f) rank 3
+# ---------------------------------------------------------------------------
+
+def config_tables():
+    import glob
+    import tempfile
+    out = []
+    for path in sorted(glob.glob("/root/reference/pkg/configs/*.cfg")):
+        cfg = R.load_config(path)
+        if cfg.problem == "euler":
+            continue      # outside the B200 path
+        if cfg.sweep is not None:
+            res = R.run_sweep(cfg)
+            table, runs = res.table, res.runs
+        else:
+            run = R.run_experiment(cfg)
+            table, runs = R.experiment_table(run), [run]
+        with tempfile.TemporaryDirectory() as d:
+            csv = os.path.join(d, "t.csv")
+            R.emit_csv(table, csv)
+            text = open(csv).read()
+        fields = {k: (list(v) if isinstance(v, tuple) else v)
+                  for k, v in dataclasses.asdict(cfg).items()}
+        out.append(dict(name=os.path.basename(path)[:-4], config=fields, csv=text,
+                        columns=list(table.columns),
+                        level_dts=[list(r.level_dts) for r in runs],
+                        level_cfls=[list(r.level_cfls) for r in runs],
+                        max_speed=[r.serial.max_speed for r in runs],
+                        diverged_at=[r.record.diverged_at for r in runs]))
+        print(f"{out[-1]['name']}: {len(runs)} columns")
+    with open(os.path.join(HERE, "config_tables.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 if __name__ == "__main__":
     import sys as _sys
-    which = _sys.argv[1:] or ["phi", "mgrit", "lf", "sw"]
+    which = _sys.argv[1:] or ["phi", "mgrit", "lf", "sw", "configs"]
+    if "configs" in which:
+        config_tables()
     if "sw" in which:
         sw_vectors()
         sw_mgrit_cases()
