@@ -56,9 +56,17 @@ extern "C" {
  * 2*nx, nx <= 2048, candidate sums always in the 2-lane order (the
  * characteristic windows are fresh contiguous arrays in the reference). */
 #define MGP_MODEL_SHALLOW_WATER 2
+/* Euler (models.py:214-308): state (rho, rho u, E), ideal gas gamma; rows of
+ * 3*nx, nx <= 2048; left eigenvectors = inv(right) by LU with partial
+ * pivoting (the reference's np.linalg.inv agrees to rounding). */
+#define MGP_MODEL_EULER 3
 
-/* bits OR-ed into *mgp_sweep_args.status where the reference raises */
-#define MGP_STATUS_NONPOSITIVE_DEPTH 1   /* PhysicalStateError, models.py:147-153 */
+/* bits OR-ed into *mgp_sweep_args.status where the reference raises
+ * PhysicalStateError */
+#define MGP_STATUS_NONPOSITIVE_DEPTH 1      /* models.py:147-153 */
+#define MGP_STATUS_NONPOSITIVE_DENSITY 2    /* models.py:228-232 */
+#define MGP_STATUS_NONPOSITIVE_PRESSURE 4   /* models.py:235-238 */
+#define MGP_STATUS_ROE_NONHYPERBOLIC 8      /* models.py:290-293 */
 
 /* NumPy candidate-sum order of weno.py:175:
  * SEQ when advance() received >= 2 fields, LANE2 for a single field. */
@@ -108,6 +116,10 @@ typedef struct mgp_phi {
     int32_t repeats;    /* >= 1: Phi = inner^repeats (ComposedStepper,
                            stepper.py:170-188); 1 otherwise                    */
     double gravity;     /* shallow water: g > 0 (models.py:139-143)            */
+    double gamma;       /* Euler: gamma > 1 (models.py:219-223)                */
+    int32_t characteristic;  /* systems: 1 characteristic-field WENO, 0 per
+                                component (WenoConfig.characteristic)      */
+    int32_t reserved;
 } mgp_phi;
 
 /*

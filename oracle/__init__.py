@@ -30,13 +30,20 @@ _LIB_PATH = os.path.join(_HERE, "libphi_oracle.so")
 MODEL_BURGERS = 0
 MODEL_ADVECTION = 1
 MODEL_SHALLOW_WATER = 2
+MODEL_EULER = 3
 _MODELS = {"burgers": MODEL_BURGERS, "advection": MODEL_ADVECTION,
-           "shallow-water": MODEL_SHALLOW_WATER}
+           "shallow-water": MODEL_SHALLOW_WATER, "euler": MODEL_EULER}
+_NCOMP = {MODEL_BURGERS: 1, MODEL_ADVECTION: 1, MODEL_SHALLOW_WATER: 2, MODEL_EULER: 3}
 
 
 class PhysicalStateOracleError(ValueError):
-    """The oracle met a non-positive depth (the reference raises
-    PhysicalStateError there, models.py:147-153)."""
+    """The oracle met an inadmissible state (the reference raises
+    PhysicalStateError there, models.py:147-153, 228-238, 290-293); ``bits``:
+    1 depth, 2 density, 4 pressure, 8 Roe average."""
+
+    def __init__(self, bits: int):
+        super().__init__(f"inadmissible state (bits {bits})")
+        self.bits = bits
 SUM_SEQ = 0
 SUM_LANE2 = 1
 
@@ -48,7 +55,8 @@ class OraParams(ctypes.Structure):
                 ("eps", ctypes.c_double), ("speed", ctypes.c_double),
                 ("scheme", ctypes.c_int32), ("lf_order", ctypes.c_int32),
                 ("m_eff", ctypes.c_int32), ("repeats", ctypes.c_int32),
-                ("gravity", ctypes.c_double)]
+                ("gravity", ctypes.c_double), ("gamma", ctypes.c_double),
+                ("characteristic", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None
@@ -90,14 +98,16 @@ def _ptr(a):
 
 def make_params(*, model="burgers", k=2, rk_order=3, dt=1e-3, dx=1.0 / 64,
                 eps=1e-6, speed=1.0, regime=SUM_SEQ, scheme=0, lf_order=0, m_eff=1,
-                repeats=1, gravity=9.81) -> OraParams:
+                repeats=1, gravity=9.81, gamma=5.0 / 3.0,
+                characteristic=True) -> OraParams:
     """scheme 0: RK over WENO/LF; 1: one-step LF (matched-lf-fine,
     rediscretized-lf), 2: matched coarse LF of order lf_order emulating m_eff
     fine steps (dt = the step the formula multiplies, see include/mgrit_phi.h);
     repeats: ComposedStepper count."""
     return OraParams(_MODELS[model], int(k), int(rk_order), int(regime), float(dt),
                      float(dx), float(eps), float(speed), int(scheme), int(lf_order),
-                     int(m_eff), int(repeats), float(gravity))
+                     int(m_eff), int(repeats), float(gravity), float(gamma),
+                     int(bool(characteristic)), 0)
 
 
 def regime_for_shape(shape) -> int:
@@ -114,7 +124,7 @@ def phi_apply(params: OraParams, u: np.ndarray, g: np.ndarray | None = None,
     """Apply Phi (+ g) to every (D, N) field of u; shape preserved."""
     u = np.ascontiguousarray(u, dtype=np.float64)
     nx = u.shape[-1]
-    row = nx * (2 if params.model == MODEL_SHALLOW_WATER else 1)
+    row = nx * _NCOMP[params.model]
     batch = u.size // row
     out = np.empty_like(u)
     gp = None
@@ -123,8 +133,8 @@ def phi_apply(params: OraParams, u: np.ndarray, g: np.ndarray | None = None,
         gp = _ptr(g)
     rc = lib().ora_phi_apply(ctypes.byref(params), _ptr(u), row, gp, row,
                              _ptr(out), row, batch, nx, int(nthreads))
-    if rc == 3:
-        raise PhysicalStateOracleError("non-positive depth")
+    if rc >= 3:
+        raise PhysicalStateOracleError(rc - 2)
     if rc != 0:
         raise ValueError(f"ora_phi_apply failed with status {rc}")
     return out
@@ -140,6 +150,8 @@ def march(params: OraParams, u: np.ndarray, g: np.ndarray | None,
         assert g.flags.c_contiguous and g.dtype == np.float64
         gp = _ptr(g)
     rc = lib().ora_march(ctypes.byref(params), _ptr(u), gp, int(n_steps), nx)
+    if rc >= 3:
+        raise PhysicalStateOracleError(rc - 2)
     if rc != 0:
         raise ValueError(f"ora_march failed with status {rc}")
 
@@ -160,8 +172,9 @@ class OracleStepper:
 
     def __init__(self, *, model="burgers", k=2, rk_order=3, dt, dx,
                  eps=1e-6, speed=1.0, nthreads=0, scheme=0, lf_order=0, m_eff=1,
-                 repeats=1, formula_dt=None, gravity=9.81):
-        self.gravity = gravity
+                 repeats=1, formula_dt=None, gravity=9.81, gamma=5.0 / 3.0,
+                 characteristic=True):
+        self.gravity, self.gamma, self.characteristic = gravity, gamma, characteristic
         self.model, self.k, self.order = model, k, rk_order
         self.dt, self.dx, self.eps, self.speed = dt, dx, eps, speed
         self.nthreads = nthreads
@@ -173,7 +186,8 @@ class OracleStepper:
                            dt=self.formula_dt, dx=self.dx, eps=self.eps,
                            speed=self.speed, regime=regime, scheme=self.scheme,
                            lf_order=self.lf_order, m_eff=self.m_eff,
-                           repeats=self.repeats, gravity=self.gravity)
+                           repeats=self.repeats, gravity=self.gravity,
+                           gamma=self.gamma, characteristic=self.characteristic)
 
     def advance(self, u):
         u = np.asarray(u, dtype=np.float64)

@@ -44,6 +44,12 @@
 #define ORA_MODEL_BURGERS 0
 #define ORA_MODEL_ADVECTION 1
 #define ORA_MODEL_SHALLOW_WATER 2   /* D = 2: (h, hu), characteristic WENO */
+#define ORA_MODEL_EULER 3           /* D = 3: (rho, rho u, E)               */
+/* bad_state bits (the reference's PhysicalStateError cases) */
+#define ORA_BAD_DEPTH 1       /* models.py:147-153 */
+#define ORA_BAD_DENSITY 2     /* models.py:228-232 */
+#define ORA_BAD_PRESSURE 4    /* models.py:235-238 */
+#define ORA_BAD_ROE 8         /* models.py:290-293 */
 #define ORA_SUM_SEQ 0
 #define ORA_SUM_LANE2 1
 
@@ -58,9 +64,14 @@ typedef struct {
     int32_t m_eff;     /* matched: fine steps emulated                        */
     int32_t repeats;   /* composition count (ComposedStepper), >= 1           */
     double gravity;    /* shallow water g                                     */
+    double gamma;      /* Euler ratio of specific heats                       */
+    int32_t characteristic;  /* systems: 1 characteristic, 0 componentwise  */
+    int32_t reserved;
 } ora_params;
 
-static int ncomp(const ora_params *p) { return p->model == ORA_MODEL_SHALLOW_WATER ? 2 : 1; }
+static int ncomp(const ora_params *p) {
+    return p->model == ORA_MODEL_SHALLOW_WATER ? 2 : (p->model == ORA_MODEL_EULER ? 3 : 1);
+}
 
 /* ---- exact rational tables, weno.py:43-86.  IEEE division of the small
  * integers gives the correctly rounded double, i.e. float(Fraction(p, q)). */
@@ -255,39 +266,162 @@ static void rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
     }
 }
 
-/* ---- shallow water (models.py:136-211), characteristic WENO
- * (weno.py:222-233), LF or Roe flux (flux.py:70-126).  State (h, hu),
- * component-major rows of nx.  Checked against the reference bit for bit
- * (tests/golden/make_golden.py): the characteristic windows are einsum
- * outputs (contiguous), so the candidate sums always use the 2-lane order;
- * the 2-term projections accumulate from +0 in index order. */
-static int sw_dv(ora_work *wk, double h, double hu, double *vel) {
-    if (h <= 0.0) wk->bad_state = 1;          /* PhysicalStateError */
-    *vel = hu / h;
-    return 0;
+/* ---- systems: shallow water (models.py:136-211) and Euler (models.py:
+ * 214-308); characteristic WENO (weno.py:203-233), LF or Roe flux
+ * (flux.py:70-126).  States are component-major rows of D*nx.  Checked
+ * against the reference bit for bit for shallow water; for Euler the left
+ * eigenvectors are np.linalg.inv of the right ones (models.py:270), restated
+ * by inv3() below (LU with partial pivoting), which agrees with LAPACK to
+ * rounding -- everything else is pinned bit for bit by running the
+ * reference with inv3 substituted (tests/golden/make_golden.py "euler").
+ * The einsum contractions over the component axis accumulate in two lanes
+ * from +0 -- (0 + x0 + x2) + (0 + x1) -- (lane2(), verified per call site
+ * against the reference); the characteristic windows are fresh contiguous
+ * arrays, so their candidate sums use the 2-lane order too. */
+static double lane2(const double *x, int n) {
+    double ev = 0.0, od = 0.0;
+    for (int i = 0; i < n; ++i) {
+        if (i & 1) od = od + x[i];
+        else ev = ev + x[i];
+    }
+    return ev + od;
 }
 
-static void sw_eigen(ora_work *wk, double g, double h, double hu, double R[2][2], double L[2][2]) {
-    double vel;
-    sw_dv(wk, h, hu, &vel);
-    const double c = sqrt(g * h);
-    const double inv2c = 0.5 / c;
-    R[0][0] = 1.0; R[0][1] = 1.0; R[1][0] = vel - c; R[1][1] = vel + c;
-    L[0][0] = (vel + c) * inv2c; L[0][1] = -1.0 * inv2c;
-    L[1][0] = (-(vel - c)) * inv2c; L[1][1] = 1.0 * inv2c;
+typedef struct {
+    double lam[3];
+    double R[3][3];   /* columns: right eigenvectors */
+    double L[3][3];   /* rows: left eigenvectors     */
+} ora_eig;
+
+/* np.linalg.inv for 3x3: LU with partial pivoting (first maximal |pivot|),
+ * multipliers scaled by the reciprocal pivot, rank-1 updates, then forward
+ * (unit lower) and backward (dividing by the pivot) substitution of each
+ * column of P I, skipping zero entries -- LAPACK dgetf2/dgetrs order */
+static void inv3(const double A[3][3], double X[3][3]) {
+    double a[3][3];
+    int perm[3] = {0, 1, 2};
+    memcpy(a, A, sizeof a);
+    for (int j = 0; j < 3; ++j) {
+        int pv = j;
+        double best = fabs(a[j][j]);
+        for (int i = j + 1; i < 3; ++i)
+            if (fabs(a[i][j]) > best) { best = fabs(a[i][j]); pv = i; }
+        if (pv != j) {
+            for (int c = 0; c < 3; ++c) { double t = a[j][c]; a[j][c] = a[pv][c]; a[pv][c] = t; }
+            int t = perm[j]; perm[j] = perm[pv]; perm[pv] = t;
+        }
+        const double rp = 1.0 / a[j][j];
+        for (int i = j + 1; i < 3; ++i) a[i][j] = a[i][j] * rp;
+        for (int i = j + 1; i < 3; ++i)
+            for (int c = j + 1; c < 3; ++c) a[i][c] = a[i][c] - a[i][j] * a[j][c];
+    }
+    for (int col = 0; col < 3; ++col) {
+        double b[3];
+        for (int i = 0; i < 3; ++i) b[i] = perm[i] == col ? 1.0 : 0.0;
+        for (int kk = 0; kk < 3; ++kk)
+            if (b[kk] != 0.0)
+                for (int i = kk + 1; i < 3; ++i) b[i] = b[i] - b[kk] * a[i][kk];
+        for (int kk = 2; kk >= 0; --kk)
+            if (b[kk] != 0.0) {
+                b[kk] = b[kk] / a[kk][kk];
+                for (int i = 0; i < kk; ++i) b[i] = b[i] - b[kk] * a[i][kk];
+            }
+        for (int i = 0; i < 3; ++i) X[i][col] = b[i];
+    }
 }
 
-static void sw_flux(ora_work *wk, double g, const double *s, double *f) {
-    double vel;
-    sw_dv(wk, s[0], s[1], &vel);
-    f[0] = s[1];
-    f[1] = ((s[0] * vel) * vel) + (((0.5 * g) * s[0]) * s[0]);
+/* velocity (and Euler pressure) of a state, flagging inadmissible ones */
+static double sys_vel(const ora_params *p, ora_work *wk, const double *s, double *pr) {
+    if (p->model == ORA_MODEL_SHALLOW_WATER) {
+        if (s[0] <= 0.0) wk->bad_state |= ORA_BAD_DEPTH;
+        return s[1] / s[0];
+    }
+    if (s[0] <= 0.0) wk->bad_state |= ORA_BAD_DENSITY;
+    const double vel = s[1] / s[0];
+    *pr = (p->gamma - 1.0) * (s[2] - ((0.5 * s[0]) * vel) * vel);
+    if (*pr <= 0.0) wk->bad_state |= ORA_BAD_PRESSURE;
+    return vel;
 }
 
-static double sw_speed(ora_work *wk, double g, const double *s) {
-    double vel;
-    sw_dv(wk, s[0], s[1], &vel);
-    return fabs(vel) + sqrt(g * s[0]);
+/* wave speed c of a state with velocity vel (and pressure pr) */
+static double sys_c(const ora_params *p, const double *s, double pr) {
+    if (p->model == ORA_MODEL_SHALLOW_WATER) return sqrt(p->gravity * s[0]);
+    return sqrt((p->gamma * pr) / s[0]);
+}
+
+static void sys_flux(const ora_params *p, ora_work *wk, const double *s, double *f) {
+    double pr = 0.0;
+    const double vel = sys_vel(p, wk, s, &pr);
+    if (p->model == ORA_MODEL_SHALLOW_WATER) {
+        f[0] = s[1];
+        f[1] = ((s[0] * vel) * vel) + (((0.5 * p->gravity) * s[0]) * s[0]);
+    } else {
+        f[0] = s[1];
+        f[1] = (s[1] * vel) + pr;
+        f[2] = (s[2] + pr) * vel;
+    }
+}
+
+static double sys_speed(const ora_params *p, ora_work *wk, const double *s) {
+    double pr = 0.0;
+    const double vel = sys_vel(p, wk, s, &pr);
+    return fabs(vel) + sys_c(p, s, pr);
+}
+
+static void sys_eigenvalues(const ora_params *p, ora_work *wk, const double *s, double *lam) {
+    double pr = 0.0;
+    const double vel = sys_vel(p, wk, s, &pr);
+    const double c = sys_c(p, s, pr);
+    if (p->model == ORA_MODEL_SHALLOW_WATER) {
+        lam[0] = vel - c; lam[1] = vel + c;
+    } else {
+        lam[0] = vel - c; lam[1] = vel; lam[2] = vel + c;
+    }
+}
+
+/* eigen structure from (vel, c[, enthalpy]) -- models.py:159-176, 262-271 */
+static void sys_eigen_from(const ora_params *p, double vel, double c, double H, ora_eig *e) {
+    if (p->model == ORA_MODEL_SHALLOW_WATER) {
+        const double inv2c = 0.5 / c;
+        e->lam[0] = vel - c; e->lam[1] = vel + c;
+        e->R[0][0] = 1.0; e->R[0][1] = 1.0; e->R[1][0] = vel - c; e->R[1][1] = vel + c;
+        e->L[0][0] = (vel + c) * inv2c; e->L[0][1] = -1.0 * inv2c;
+        e->L[1][0] = (-(vel - c)) * inv2c; e->L[1][1] = 1.0 * inv2c;
+        return;
+    }
+    e->lam[0] = vel - c; e->lam[1] = vel; e->lam[2] = vel + c;
+    e->R[0][0] = 1.0; e->R[0][1] = 1.0; e->R[0][2] = 1.0;
+    e->R[1][0] = vel - c; e->R[1][1] = vel; e->R[1][2] = vel + c;
+    e->R[2][0] = H - vel * c; e->R[2][1] = (0.5 * vel) * vel; e->R[2][2] = H + vel * c;
+    inv3(e->R, e->L);
+}
+
+static void sys_eigen_cell(const ora_params *p, ora_work *wk, const double *s, ora_eig *e) {
+    double pr = 0.0;
+    const double vel = sys_vel(p, wk, s, &pr);
+    const double c = sys_c(p, s, pr);
+    const double H = p->model == ORA_MODEL_EULER ? (s[2] + pr) / s[0] : 0.0;
+    sys_eigen_from(p, vel, c, H, e);
+}
+
+/* Roe linearisation (models.py:178-200, 280-300) */
+static void sys_eigen_roe(const ora_params *p, ora_work *wk, const double *l, const double *r,
+                          ora_eig *e) {
+    double pl = 0.0, prr = 0.0;
+    const double vl = sys_vel(p, wk, l, &pl), vr = sys_vel(p, wk, r, &prr);
+    const double sl = sqrt(l[0]), sr = sqrt(r[0]);
+    if (p->model == ORA_MODEL_SHALLOW_WATER) {
+        const double hh = 0.5 * (l[0] + r[0]);
+        const double uh = (sl * vl + sr * vr) / (sl + sr);
+        sys_eigen_from(p, uh, sqrt(p->gravity * hh), 0.0, e);
+        return;
+    }
+    const double hl = (l[2] + pl) / l[0], hr = (r[2] + prr) / r[0];
+    const double uh = (sl * vl + sr * vr) / (sl + sr);
+    const double Hh = (sl * hl + sr * hr) / (sl + sr);
+    const double csq = (p->gamma - 1.0) * (Hh - (0.5 * uh) * uh);
+    if (csq <= 0.0) wk->bad_state |= ORA_BAD_ROE;
+    sys_eigen_from(p, uh, sqrt(csq), Hh, e);
 }
 
 static double entropy_fix1(double lh, double ll, double lr) {
@@ -298,83 +432,80 @@ static double entropy_fix1(double lh, double ll, double lr) {
     return (alam < delta) ? 0.5 * ((lh * lh) / delta + delta) : alam;
 }
 
-static void sw_rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
-                         const double *v, double *A) {
+static void sys_rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
+                          const double *v, double *A) {
     const int64_t nx = wk->nx;
-    const int k = t->k, W = 2 * k + 1;
-    const double g = p->gravity;
-    double *sl = wk->ul, *sr = wk->ur, *F = wk->F;   /* component-major (2, nx) */
+    const int k = t->k, W = 2 * k + 1, D = ncomp(p);
+    double *sl = wk->ul, *sr = wk->ur, *F = wk->F;   /* component-major (D, nx) */
     for (int64_t i = 0; i < nx; ++i) {
-        double R0[2][2], L0[2][2], R1[2][2], L1[2][2];
         const int64_t ip = (i + 1) % nx;
-        sw_eigen(wk, g, v[i], v[nx + i], R0, L0);
-        sw_eigen(wk, g, v[ip], v[nx + ip], R1, L1);
+        ora_eig e[2];
+        if (p->characteristic) {
+            double s0[3], s1[3];
+            for (int d = 0; d < D; ++d) { s0[d] = v[d * nx + i]; s1[d] = v[d * nx + ip]; }
+            sys_eigen_cell(p, wk, s0, &e[0]);
+            sys_eigen_cell(p, wk, s1, &e[1]);
+        }
         for (int side = 0; side < 2; ++side) {
-            double (*Lv)[2] = side == 0 ? L0 : L1;
-            double (*Rv)[2] = side == 0 ? R0 : R1;
-            double ch[2][7], rec[2];
+            double win[3][7], rec[3];
             for (int s2 = 0; s2 < W; ++s2) {
                 /* left window: cells i-k+s2; right window: cells i+1+k-s2 */
                 const int64_t c = side == 0 ? (i - k + s2) : (i + 1 + k - s2);
                 const int64_t cc = ((c % nx) + nx) % nx;
-                for (int q = 0; q < 2; ++q) {
-                    double acc = 0.0;
-                    acc = acc + Lv[q][0] * v[cc];
-                    acc = acc + Lv[q][1] * v[nx + cc];
-                    ch[q][s2] = acc;
-                }
+                for (int d = 0; d < D; ++d) win[d][s2] = v[d * nx + cc];
             }
-            for (int q = 0; q < 2; ++q) rec[q] = recon(t, ORA_SUM_LANE2, ch[q]);
             double *dst = side == 0 ? sl : sr;
-            for (int d = 0; d < 2; ++d) {
-                double acc = 0.0;
-                acc = acc + Rv[d][0] * rec[0];
-                acc = acc + Rv[d][1] * rec[1];
-                dst[d * nx + i] = acc;
+            if (!p->characteristic) {
+                /* (..., D, N, W) windows: >= 2 fields, sequential sums */
+                for (int d = 0; d < D; ++d) dst[d * nx + i] = recon(t, ORA_SUM_SEQ, win[d]);
+                continue;
+            }
+            const ora_eig *E = &e[side];
+            double ch[3][7];
+            double term[3];
+            for (int s2 = 0; s2 < W; ++s2)
+                for (int q = 0; q < D; ++q) {
+                    for (int d = 0; d < D; ++d) term[d] = E->L[q][d] * win[d][s2];
+                    ch[q][s2] = lane2(term, D);
+                }
+            for (int q = 0; q < D; ++q) rec[q] = recon(t, ORA_SUM_LANE2, ch[q]);
+            for (int d = 0; d < D; ++d) {
+                for (int q = 0; q < D; ++q) term[q] = E->R[d][q] * rec[q];
+                dst[d * nx + i] = lane2(term, D);
             }
         }
     }
     if (p->scheme == 3) {                       /* Roe, flux.py:91-126 */
         for (int64_t i = 0; i < nx; ++i) {
-            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
-            double vl, vr;
-            sw_dv(wk, l[0], l[1], &vl);
-            sw_dv(wk, r[0], r[1], &vr);
-            const double s_l = sqrt(l[0]), s_r = sqrt(r[0]);
-            const double hh = 0.5 * (l[0] + r[0]);
-            const double uh = (s_l * vl + s_r * vr) / (s_l + s_r);
-            const double ch = sqrt(g * hh);
-            const double lam[2] = {uh - ch, uh + ch};
-            const double inv2c = 0.5 / ch;
-            const double Rr[2][2] = {{1.0, 1.0}, {lam[0], lam[1]}};
-            const double Lr[2][2] = {{(uh + ch) * inv2c, -1.0 * inv2c},
-                                     {(-(uh - ch)) * inv2c, 1.0 * inv2c}};
-            const double jump[2] = {r[0] - l[0], r[1] - l[1]};
-            const double cl = sqrt(g * l[0]), cr = sqrt(g * r[0]);
-            const double ll[2] = {vl - cl, vl + cl}, lr[2] = {vr - cr, vr + cr};
-            double ss[2];
-            for (int kk = 0; kk < 2; ++kk) {
-                double acc = 0.0;
-                acc = acc + Lr[kk][0] * jump[0];
-                acc = acc + Lr[kk][1] * jump[1];
-                ss[kk] = entropy_fix1(lam[kk], ll[kk], lr[kk]) * acc;
+            double l[3], r[3], jump[3], lamL[3], lamR[3], fl[3], fr[3], ss[3];
+            for (int d = 0; d < D; ++d) {
+                l[d] = sl[d * nx + i];
+                r[d] = sr[d * nx + i];
+                jump[d] = r[d] - l[d];
             }
-            double fl[2], fr[2];
-            sw_flux(wk, g, l, fl);
-            sw_flux(wk, g, r, fr);
-            for (int d = 0; d < 2; ++d) {
-                double acc = 0.0;
-                acc = acc + ss[0] * Rr[d][0];
-                acc = acc + ss[1] * Rr[d][1];
-                F[d * nx + i] = (0.5 * (fl[d] + fr[d])) - (0.5 * acc);
+            ora_eig e;
+            sys_eigen_roe(p, wk, l, r, &e);
+            sys_eigenvalues(p, wk, l, lamL);
+            sys_eigenvalues(p, wk, r, lamR);
+            double term[3];
+            for (int kk = 0; kk < D; ++kk) {
+                for (int d = 0; d < D; ++d) term[d] = e.L[kk][d] * jump[d];
+                ss[kk] = entropy_fix1(e.lam[kk], lamL[kk], lamR[kk]) * lane2(term, D);
+            }
+            sys_flux(p, wk, l, fl);
+            sys_flux(p, wk, r, fr);
+            for (int d = 0; d < D; ++d) {
+                for (int kk = 0; kk < D; ++kk) term[kk] = ss[kk] * e.R[d][kk];
+                F[d * nx + i] = (0.5 * (fl[d] + fr[d])) - (0.5 * lane2(term, D));
             }
         }
     } else {                                    /* global LF, flux.py:70-88 */
         double ml = 0.0, mr = 0.0;
         int nan = 0;
         for (int64_t i = 0; i < nx; ++i) {
-            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
-            const double a = sw_speed(wk, g, l), b = sw_speed(wk, g, r);
+            double l[3], r[3];
+            for (int d = 0; d < D; ++d) { l[d] = sl[d * nx + i]; r[d] = sr[d * nx + i]; }
+            const double a = sys_speed(p, wk, l), b = sys_speed(p, wk, r);
             if (isnan(a) || isnan(b)) nan = 1;
             if (a > ml) ml = a;
             if (b > mr) mr = b;
@@ -382,15 +513,15 @@ static void sw_rhs_field(const ora_params *p, const ora_tables *t, ora_work *wk,
         const double alpha = nan ? NAN : (ml > mr ? ml : mr);
         const double ha = 0.5 * alpha;
         for (int64_t i = 0; i < nx; ++i) {
-            const double l[2] = {sl[i], sl[nx + i]}, r[2] = {sr[i], sr[nx + i]};
-            double fl[2], fr[2];
-            sw_flux(wk, g, l, fl);
-            sw_flux(wk, g, r, fr);
-            for (int d = 0; d < 2; ++d)
+            double l[3], r[3], fl[3], fr[3];
+            for (int d = 0; d < D; ++d) { l[d] = sl[d * nx + i]; r[d] = sr[d * nx + i]; }
+            sys_flux(p, wk, l, fl);
+            sys_flux(p, wk, r, fr);
+            for (int d = 0; d < D; ++d)
                 F[d * nx + i] = (0.5 * (fl[d] + fr[d])) - (ha * (r[d] - l[d]));
         }
     }
-    for (int d = 0; d < 2; ++d)
+    for (int d = 0; d < D; ++d)
         for (int64_t i = 0; i < nx; ++i) {
             const double fm = F[d * nx + (i == 0 ? nx - 1 : i - 1)];
             A[d * nx + i] = (-(F[d * nx + i] - fm)) / p->dx;
@@ -465,7 +596,7 @@ static void phi_field(const ora_params *p, const ora_tables *t, ora_work *wk,
 
 static void any_rhs(const ora_params *p, const ora_tables *t, ora_work *wk,
                     const double *v, double *A) {
-    if (p->model == ORA_MODEL_SHALLOW_WATER) sw_rhs_field(p, t, wk, v, A);
+    if (ncomp(p) > 1) sys_rhs_field(p, t, wk, v, A);
     else rhs_field(p, t, wk, v, A);
 }
 
@@ -512,9 +643,10 @@ static int check_params(const ora_params *p, int64_t nx) {
     if (p->scheme != 0 && p->scheme != 3) return 1;
     if (p->scheme == 3 && p->model == ORA_MODEL_ADVECTION) return 1;
     if (p->model == ORA_MODEL_SHALLOW_WATER && !(p->gravity > 0.0)) return 1;
+    if (p->model == ORA_MODEL_EULER && !(p->gamma > 1.0)) return 1;
     if (p->k < 0 || p->k > 3) return 1;
     if (p->rk_order < 0 || p->rk_order > 3) return 1;
-    if (p->model < ORA_MODEL_BURGERS || p->model > ORA_MODEL_SHALLOW_WATER) return 1;
+    if (p->model < ORA_MODEL_BURGERS || p->model > ORA_MODEL_EULER) return 1;
     if (p->regime != ORA_SUM_SEQ && p->regime != ORA_SUM_LANE2) return 1;
     if (nx < 2 * p->k + 1) return 1;
     return 0;
@@ -553,7 +685,7 @@ static void *ora_worker(void *arg) {
     }
     if (wk.bad_state) {
         pthread_mutex_lock(&job->lock);
-        job->bad = 1;
+        job->bad |= wk.bad_state;
         pthread_mutex_unlock(&job->lock);
     }
     work_free(&wk);
@@ -571,7 +703,8 @@ int ora_max_threads(void) {
  * state.  Fields are independent and are spread over nthreads POSIX threads
  * (nthreads <= 0: one per online core).  Rows hold ncomp(model) * nx doubles
  * (component-major).  Returns 0, 1 on bad arguments, 2 on allocation failure,
- * 3 when a non-positive depth was met (the reference's PhysicalStateError).
+ * 2 + (ORA_BAD_* bits) when an inadmissible state was met (the reference's
+ * PhysicalStateError).
  */
 int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
                   const double *g, int64_t g_stride, double *out,
@@ -585,7 +718,7 @@ int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
                    0, PTHREAD_MUTEX_INITIALIZER, 0, 0};
     if (nthreads == 1) {
         ora_worker(&job);
-        return job.err ? 2 : (job.bad ? 3 : 0);
+        return job.err ? 2 : (job.bad ? 2 + job.bad : 0);
     }
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
     if (!th) return 2;
@@ -595,7 +728,7 @@ int ora_phi_apply(const ora_params *p, const double *u, int64_t u_stride,
     if (started == 0) ora_worker(&job);
     for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
     free(th);
-    return job.err ? 2 : (job.bad ? 3 : 0);
+    return job.err ? 2 : (job.bad ? 2 + job.bad : 0);
 }
 
 /*
@@ -615,5 +748,5 @@ int ora_march(const ora_params *p, double *u, const double *g, int64_t n_steps,
         phi_field(p, &t, &wk, u + (i - 1) * len, g ? g + i * len : NULL, u + i * len);
     const int bad = wk.bad_state;
     work_free(&wk);
-    return bad ? 3 : 0;
+    return bad ? 2 + bad : 0;
 }

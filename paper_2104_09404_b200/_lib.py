@@ -27,9 +27,12 @@ G_NONE, G_ZERO, G_ARRAY = 0, 1, 2
 TAIL_NONE, TAIL_PHI, TAIL_RESTRICT, TAIL_RESID = 0, 1, 2, 3
 SCHEME_RK_WENO, SCHEME_LF_ONESTEP, SCHEME_LF_MATCHED, SCHEME_RK_WENO_ROE = 0, 1, 2, 3
 GUESS_LAST_STEP, GUESS_INJECTION = 0, 1
-MODEL_BURGERS, MODEL_ADVECTION, MODEL_SHALLOW_WATER = 0, 1, 2
+MODEL_BURGERS, MODEL_ADVECTION, MODEL_SHALLOW_WATER, MODEL_EULER = 0, 1, 2, 3
 STATUS_NONPOSITIVE_DEPTH = 1
-ABI_VERSION = 2
+STATUS_NONPOSITIVE_DENSITY = 2
+STATUS_NONPOSITIVE_PRESSURE = 4
+STATUS_ROE_NONHYPERBOLIC = 8
+ABI_VERSION = 3
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,7 +51,9 @@ class MgpPhi(ctypes.Structure):
                 ("dx", ctypes.c_double), ("epsilon", ctypes.c_double),
                 ("speed", ctypes.c_double), ("scheme", ctypes.c_int32),
                 ("lf_order", ctypes.c_int32), ("m_eff", ctypes.c_int32),
-                ("repeats", ctypes.c_int32), ("gravity", ctypes.c_double)]
+                ("repeats", ctypes.c_int32), ("gravity", ctypes.c_double),
+                ("gamma", ctypes.c_double), ("characteristic", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 _P = ctypes.c_void_p
@@ -140,7 +145,7 @@ def launch_count() -> int:
 def max_nx_static(weno_k: int = 2, model: int = 0) -> int:
     """The library's mesh limits (mgp_max_nx) without loading it: 4096 cells
     per CTA, WENO5 Burgers up to 16 x 4096 over a cluster, shallow water 2048."""
-    if model == MODEL_SHALLOW_WATER:
+    if model in (MODEL_SHALLOW_WATER, MODEL_EULER):
         return 2048
     return 16 * 4096 if (weno_k == 2 and model == MODEL_BURGERS) else 4096
 

@@ -291,6 +291,7 @@ struct Consts {
     int dx_pow2, twodx_pow2;
     int lf_order, m_eff;
     double gravity;            // shallow water
+    double gamma, gm1;         // Euler: gamma, gamma - 1
 };
 
 namespace cg = cooperative_groups;
@@ -917,21 +918,23 @@ __global__ void __launch_bounds__(256) lf_kernel(const mgp_sweep_args a, const C
 }
 
 // ---------------------------------------------------------------------------
-// Shallow-water system (models.py:136-211): state (h, hu), component-major
-// rows of 2 nx.  Characteristic WENO (weno.py:222-233, flux.py:127-161): the
-// window of cell c is projected onto the left eigenvectors of cell c,
-//   L(c) = [[(u+c)/2c, -1/2c], [-(u-c)/2c, 1/2c]],  c = sqrt(g h),
-// each characteristic field is reconstructed (left state of interface c and
-// right state of interface c-1 from the same window, shared beta products),
-// and mapped back with R(c) = [[1, 1], [u-c, u+c]].  The einsum projections
-// accumulate from +0 in index order; the candidate sums use the 2-lane order
-// (the characteristic windows are contiguous arrays in the reference).  Flux:
-// global LF (alpha = NaN-propagating max of |u| + sqrt(g h) over both
-// interface states) or Roe with the Harten-Hyman entropy fix per
-// characteristic field (flux.py:91-126, models.py:185-211).  Depth <= 0 in any
-// state the reference passes through _depth_velocity raises
-// PhysicalStateError there (models.py:147-153); here it sets
-// MGP_STATUS_NONPOSITIVE_DEPTH in *status and the sweep completes.
+// Hyperbolic systems: shallow water (D = 2, models.py:136-211) and Euler
+// (D = 3, models.py:214-308); component-major rows of D nx.
+// Characteristic WENO (weno.py:203-233, flux.py:127-161): the window of cell
+// c is projected onto the left eigenvectors L(c) of cell c, every
+// characteristic field is reconstructed (left state of interface c and right
+// state of interface c-1 from the same window, sharing the beta products)
+// and mapped back with the right eigenvectors R(c).  Shallow water has L in
+// closed form (models.py:159-170); Euler takes L = inv(R) (models.py:270),
+// computed by inv3() -- LU with partial pivoting in LAPACK's operation order
+// (the reference's np.linalg.inv agrees with it to rounding).
+// Every contraction over the component axis is summed like the reference's
+// einsum: two lanes from +0, (0 + t0 + t2) + (0 + t1); candidate sums use
+// the 2-lane order (componentwise reconstruction, characteristic = false:
+// the sequential order).  Flux: global LF (alpha = NaN-propagating max of
+// |u| + c over both interface states) or Roe with the Harten-Hyman entropy
+// fix per wave (flux.py:91-126).  States the reference rejects with
+// PhysicalStateError set MGP_STATUS_* bits in *status; the sweep completes.
 // One CTA per field, whole field in shared memory (nx <= kMaxSysNx).
 // ---------------------------------------------------------------------------
 constexpr int kMaxSysNx = 2048;
@@ -944,24 +947,106 @@ __device__ __forceinline__ double entropy_fix(double lh, double ll, double lr) {
     return (alam < delta) ? 0.5 * ((lh * lh) / delta + delta) : alam;
 }
 
-template <int K, bool ROE>
+// the reference einsum's component-axis sum
+template <int D>
+__device__ __forceinline__ double lane_sum(const double *t) {
+    double ev = 0.0, od = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+        if (i & 1) od = od + t[i];
+        else ev = ev + t[i];
+    }
+    return ev + od;
+}
+
+// np.linalg.inv of a 3x3 (models.py:270): LU with partial pivoting (first
+// maximal |pivot|), multipliers scaled by the reciprocal pivot, rank-1
+// updates, then unit-lower forward and pivot-dividing backward substitution
+// of each column of P I, skipping zero entries (LAPACK dgetf2 / dgetrs)
+__device__ __forceinline__ void inv3(const double (&A)[3][3], double (&X)[3][3]) {
+    double a[3][3];
+    int perm[3] = {0, 1, 2};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) a[i][c] = A[i][c];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        int pv = j;
+        double best = fabs(a[j][j]);
+#pragma unroll
+        for (int i = j + 1; i < 3; ++i)
+            if (fabs(a[i][j]) > best) { best = fabs(a[i][j]); pv = i; }
+        // row swap without dynamic register indexing
+#pragma unroll
+        for (int i = j + 1; i < 3; ++i)
+            if (pv == i) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double t = a[j][c];
+                    a[j][c] = a[i][c];
+                    a[i][c] = t;
+                }
+                const int t = perm[j];
+                perm[j] = perm[i];
+                perm[i] = t;
+            }
+        const double rp = 1.0 / a[j][j];
+#pragma unroll
+        for (int i = j + 1; i < 3; ++i) a[i][j] = a[i][j] * rp;
+#pragma unroll
+        for (int i = j + 1; i < 3; ++i)
+#pragma unroll
+            for (int c = j + 1; c < 3; ++c) a[i][c] = a[i][c] - a[i][j] * a[j][c];
+    }
+#pragma unroll
+    for (int col = 0; col < 3; ++col) {
+        double b[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) b[i] = perm[i] == col ? 1.0 : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk)
+            if (b[kk] != 0.0)
+#pragma unroll
+                for (int i = kk + 1; i < 3; ++i) b[i] = b[i] - b[kk] * a[i][kk];
+#pragma unroll
+        for (int kk = 2; kk >= 0; --kk)
+            if (b[kk] != 0.0) {
+                b[kk] = b[kk] / a[kk][kk];
+#pragma unroll
+                for (int i = 0; i < kk; ++i) b[i] = b[i] - b[kk] * a[i][kk];
+            }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) X[i][col] = b[i];
+    }
+}
+
+template <int D>
+struct Eig {
+    double lam[D];
+    double R[D][D];
+    double L[D][D];
+};
+
+template <int K, bool ROE, int D>
 struct SysField {
     static constexpr int HALO = 0;   // halos are maintained by load/put
     static constexpr int H = K;      // window reach
     int nx, pitch;                   // cells; per-component stride of s_u
+    bool charwise;                   // characteristic reconstruction
     double *s_u;    // stage input: component d, cell c at s_u[d*pitch + H + c]
     double *s_u0;   // RK base, element e = d*nx + c
     double *s_L;    // left states at interface i (e = d*nx + i), then fluxes
     double *s_R;    // right states at interface i, then results
     unsigned long long *s_red;   // [32] per-warp alpha bits
     int32_t *status;
-    bool bad;
+    int bad;
 
     __device__ __forceinline__ double cellv(int d, int c) const {
         return s_u[d * pitch + H + c];
     }
     __device__ __forceinline__ void load(int e, double v) {
-        const int d = e >= nx ? 1 : 0;
+        const int d = e / nx;
         const int c = e - d * nx;
         double *row = s_u + d * pitch + H;
         row[c] = v;
@@ -972,12 +1057,61 @@ struct SysField {
     __device__ __forceinline__ double result(int e) const { return s_R[e]; }
     __device__ __forceinline__ void sync() { __syncthreads(); }
 
-    __device__ __forceinline__ void check(double h) {
-        if (h <= 0.0) bad = true;
+    // velocity (and Euler pressure) of a state; flags inadmissible states
+    __device__ __forceinline__ double vel_of(const Consts &k, const double *s, double &p) {
+        if (D == 2) {
+            if (s[0] <= 0.0) bad |= MGP_STATUS_NONPOSITIVE_DEPTH;
+            p = 0.0;
+            return s[1] / s[0];
+        }
+        if (s[0] <= 0.0) bad |= MGP_STATUS_NONPOSITIVE_DENSITY;
+        const double vel = s[1] / s[0];
+        p = k.gm1 * (s[D - 1] - ((0.5 * s[0]) * vel) * vel);
+        if (p <= 0.0) bad |= MGP_STATUS_NONPOSITIVE_PRESSURE;
+        return vel;
+    }
+    __device__ __forceinline__ double c_of(const Consts &k, const double *s, double p) const {
+        return D == 2 ? sqrt(k.gravity * s[0]) : sqrt((k.gamma * p) / s[0]);
+    }
+    __device__ __forceinline__ void flux(const Consts &k, const double *s, double *f) {
+        double p;
+        const double vel = vel_of(k, s, p);
+        f[0] = s[1];
+        if (D == 2) {
+            f[1] = ((s[0] * vel) * vel) + (((0.5 * k.gravity) * s[0]) * s[0]);
+        } else {
+            f[1] = (s[1] * vel) + p;
+            f[D - 1] = (s[D - 1] + p) * vel;
+        }
+    }
+    __device__ __forceinline__ void eigen_from(double vel, double c, double Hh, Eig<D> &e) const {
+        if (D == 2) {
+            const double inv2c = 0.5 / c;
+            e.lam[0] = vel - c;
+            e.lam[D - 1] = vel + c;
+            e.R[0][0] = 1.0; e.R[0][D - 1] = 1.0;
+            e.R[D - 1][0] = vel - c; e.R[D - 1][D - 1] = vel + c;
+            e.L[0][0] = (vel + c) * inv2c; e.L[0][D - 1] = -1.0 * inv2c;
+            e.L[D - 1][0] = (-(vel - c)) * inv2c; e.L[D - 1][D - 1] = 1.0 * inv2c;
+        } else {
+            double R3[3][3], L3[3][3];
+            e.lam[0] = vel - c; e.lam[1] = vel; e.lam[D - 1] = vel + c;
+            R3[0][0] = 1.0; R3[0][1] = 1.0; R3[0][2] = 1.0;
+            R3[1][0] = vel - c; R3[1][1] = vel; R3[1][2] = vel + c;
+            R3[2][0] = Hh - vel * c; R3[2][1] = (0.5 * vel) * vel; R3[2][2] = Hh + vel * c;
+            inv3(R3, L3);
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    e.R[i][j] = R3[i % 3][j % 3];
+                    e.L[i][j] = L3[i % 3][j % 3];
+                }
+        }
     }
 
-    // WENO of one characteristic window: left state (interface m) and right
-    // state (interface m-1)
+    // WENO of one window: left state (interface m) and right state (m-1)
+    template <int REG>
     __device__ __forceinline__ void recon2(const Consts &k, const double *w, double &l,
                                            double &r) const {
         double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
@@ -985,80 +1119,120 @@ struct SysField {
         for (int s2 = 0; s2 <= K; ++s2) beta_block<K, true>(w, s2, bl[s2], br[K - s2]);
 #pragma unroll
         for (int q = 0; q <= K; ++q) {
-            ql[q] = cand_left<K, MGP_SUM_LANE2>(w, q);
-            qr[q] = cand_right<K, MGP_SUM_LANE2>(w, q);
+            ql[q] = cand_left<K, REG>(w, q);
+            qr[q] = cand_right<K, REG>(w, q);
         }
         l = weno_value<K>(bl, ql, k.eps);
         r = weno_value<K>(br, qr, k.eps);
     }
 
-    // physical flux and |u| + sqrt(g h) of one interface state
-    __device__ __forceinline__ void flux(const Consts &k, double h, double hu, double &f0,
-                                         double &f1) {
-        check(h);
-        const double vel = hu / h;
-        f0 = hu;
-        f1 = ((h * vel) * vel) + (((0.5 * k.gravity) * h) * h);
-    }
-
     // interface states of every interface; returns this thread's alpha bits
     __device__ __forceinline__ unsigned long long reconstruct(const Consts &k) {
         unsigned long long m = 0;
-        const double g = k.gravity;
         for (int c = threadIdx.x; c < nx; c += blockDim.x) {
-            const double h = cellv(0, c), hu = cellv(1, c);
-            check(h);
-            const double vel = hu / h;
-            const double cs = sqrt(g * h);
-            const double inv2c = 0.5 / cs;
-            const double L00 = (vel + cs) * inv2c, L01 = -1.0 * inv2c;
-            const double L10 = (-(vel - cs)) * inv2c, L11 = 1.0 * inv2c;
-            const double R10 = vel - cs, R11 = vel + cs;
-            double w0[2 * K + 1], w1[2 * K + 1];
+            double sl[D], sr[D];
+            if (charwise) {
+                double s0[D], p;
 #pragma unroll
-            for (int s2 = 0; s2 <= 2 * K; ++s2) {
-                const double x0 = cellv(0, c - K + s2), x1 = cellv(1, c - K + s2);
-                double a0 = 0.0;
-                a0 = a0 + L00 * x0;
-                w0[s2] = a0 + L01 * x1;
-                double a1 = 0.0;
-                a1 = a1 + L10 * x0;
-                w1[s2] = a1 + L11 * x1;
+                for (int d = 0; d < D; ++d) s0[d] = cellv(d, c);
+                const double vel = vel_of(k, s0, p);
+                const double cs = c_of(k, s0, p);
+                const double Hh = D == 3 ? (s0[D - 1] + p) / s0[0] : 0.0;
+                Eig<D> e;
+                eigen_from(vel, cs, Hh, e);
+                double lrec[D], rrec[D];
+#pragma unroll
+                for (int q = 0; q < D; ++q) {
+                    double w[2 * K + 1];
+#pragma unroll
+                    for (int s2 = 0; s2 <= 2 * K; ++s2) {
+                        double t[D];
+#pragma unroll
+                        for (int d = 0; d < D; ++d) t[d] = e.L[q][d] * cellv(d, c - K + s2);
+                        w[s2] = lane_sum<D>(t);
+                    }
+                    recon2<MGP_SUM_LANE2>(k, w, lrec[q], rrec[q]);
+                }
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    double t[D], u[D];
+#pragma unroll
+                    for (int q = 0; q < D; ++q) {
+                        t[q] = e.R[d][q] * lrec[q];
+                        u[q] = e.R[d][q] * rrec[q];
+                    }
+                    sl[d] = lane_sum<D>(t);
+                    sr[d] = lane_sum<D>(u);
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    double w[2 * K + 1];
+#pragma unroll
+                    for (int s2 = 0; s2 <= 2 * K; ++s2) w[s2] = cellv(d, c - K + s2);
+                    recon2<MGP_SUM_SEQ>(k, w, sl[d], sr[d]);
+                }
             }
-            double l0, r0, l1, r1;
-            recon2(k, w0, l0, r0);
-            recon2(k, w1, l1, r1);
-            // back to conserved variables: R(c) @ (rec0, rec1)
-            double t;
-            t = 0.0;
-            t = t + 1.0 * l0;
-            const double lh = t + 1.0 * l1;
-            t = 0.0;
-            t = t + R10 * l0;
-            const double lhu = t + R11 * l1;
-            t = 0.0;
-            t = t + 1.0 * r0;
-            const double rh = t + 1.0 * r1;
-            t = 0.0;
-            t = t + R10 * r0;
-            const double rhu = t + R11 * r1;
             const int im = c == 0 ? nx - 1 : c - 1;
-            s_L[c] = lh;
-            s_L[nx + c] = lhu;
-            s_R[im] = rh;
-            s_R[nx + im] = rhu;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                s_L[d * nx + c] = sl[d];
+                s_R[d * nx + im] = sr[d];
+            }
             if (!ROE) {
-                check(lh);
-                check(rh);
-                const double sl = fabs(lhu / lh) + sqrt(g * lh);
-                const double sr = fabs(rhu / rh) + sqrt(g * rh);
-                m = umax64(m, umax64(abs_bits(sl), abs_bits(sr)));
+                double p;
+                const double vl = vel_of(k, sl, p);
+                const double al = fabs(vl) + c_of(k, sl, p);
+                const double vr = vel_of(k, sr, p);
+                const double ar = fabs(vr) + c_of(k, sr, p);
+                m = umax64(m, umax64(abs_bits(al), abs_bits(ar)));
             }
         }
         return m;
     }
 
-    __device__ __forceinline__ void rhs(const Consts &k, int last_stage_unused) {
+    __device__ __forceinline__ void roe(const Consts &k, const double *l, const double *r,
+                                        double *F) {
+        double pl, pr;
+        const double vl = vel_of(k, l, pl), vr = vel_of(k, r, pr);
+        const double sql = sqrt(l[0]), sqr = sqrt(r[0]);
+        Eig<D> e;
+        if (D == 2) {
+            const double hh = 0.5 * (l[0] + r[0]);
+            const double uh = (sql * vl + sqr * vr) / (sql + sqr);
+            eigen_from(uh, sqrt(k.gravity * hh), 0.0, e);
+        } else {
+            const double hl = (l[D - 1] + pl) / l[0], hr = (r[D - 1] + pr) / r[0];
+            const double uh = (sql * vl + sqr * vr) / (sql + sqr);
+            const double Hh = (sql * hl + sqr * hr) / (sql + sqr);
+            const double csq = k.gm1 * (Hh - (0.5 * uh) * uh);
+            if (csq <= 0.0) bad |= MGP_STATUS_ROE_NONHYPERBOLIC;
+            eigen_from(uh, sqrt(csq), Hh, e);
+        }
+        const double cl = c_of(k, l, pl), cr = c_of(k, r, pr);
+        double laml[D], lamr[D];
+        laml[0] = vl - cl; laml[D - 1] = vl + cl;
+        lamr[0] = vr - cr; lamr[D - 1] = vr + cr;
+        if (D == 3) { laml[1 % D] = vl; lamr[1 % D] = vr; }
+        double ss[D], t[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) t[d] = e.L[q][d] * (r[d] - l[d]);
+            ss[q] = entropy_fix(e.lam[q], laml[q], lamr[q]) * lane_sum<D>(t);
+        }
+        double fl[D], fr[D];
+        flux(k, l, fl);
+        flux(k, r, fr);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) t[q] = ss[q] * e.R[d][q];
+            F[d] = (0.5 * (fl[d] + fr[d])) - (0.5 * lane_sum<D>(t));
+        }
+    }
+
+    __device__ __forceinline__ void rhs(const Consts &k) {
         unsigned long long m = reconstruct(k);
         double half_alpha = 0.0;
         if (!ROE) {
@@ -1073,55 +1247,31 @@ struct SysField {
             for (int w = 1; w < nw; ++w) m = umax64(m, s_red[w]);
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         }
-        const double g = k.gravity;
         for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-            const double lh = s_L[i], lhu = s_L[nx + i];
-            const double rh = s_R[i], rhu = s_R[nx + i];
-            double fl0, fl1, fr0, fr1;
-            if (ROE) {
-                check(lh);
-                check(rh);
-                const double vl = lhu / lh, vr = rhu / rh;
-                const double sql = sqrt(lh), sqr = sqrt(rh);
-                const double hh = 0.5 * (lh + rh);
-                const double uh = (sql * vl + sqr * vr) / (sql + sqr);
-                const double ch = sqrt(g * hh);
-                const double lam0 = uh - ch, lam1 = uh + ch;
-                const double inv2c = 0.5 / ch;
-                const double Lr00 = (uh + ch) * inv2c, Lr01 = -1.0 * inv2c;
-                const double Lr10 = (-(uh - ch)) * inv2c, Lr11 = 1.0 * inv2c;
-                const double j0 = rh - lh, j1 = rhu - lhu;
-                const double cl = sqrt(g * lh), cr = sqrt(g * rh);
-                double t = 0.0;
-                t = t + Lr00 * j0;
-                t = t + Lr01 * j1;
-                const double ss0 = entropy_fix(lam0, vl - cl, vr - cr) * t;
-                t = 0.0;
-                t = t + Lr10 * j0;
-                t = t + Lr11 * j1;
-                const double ss1 = entropy_fix(lam1, vl + cl, vr + cr) * t;
-                flux(k, lh, lhu, fl0, fl1);
-                flux(k, rh, rhu, fr0, fr1);
-                t = 0.0;
-                t = t + ss0 * 1.0;
-                const double d0 = t + ss1 * 1.0;
-                t = 0.0;
-                t = t + ss0 * lam0;
-                const double d1 = t + ss1 * lam1;
-                s_L[i] = (0.5 * (fl0 + fr0)) - (0.5 * d0);
-                s_L[nx + i] = (0.5 * (fl1 + fr1)) - (0.5 * d1);
-            } else {
-                flux(k, lh, lhu, fl0, fl1);
-                flux(k, rh, rhu, fr0, fr1);
-                s_L[i] = (0.5 * (fl0 + fr0)) - (half_alpha * (rh - lh));
-                s_L[nx + i] = (0.5 * (fl1 + fr1)) - (half_alpha * (rhu - lhu));
+            double l[D], r[D], F[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                l[d] = s_L[d * nx + i];
+                r[d] = s_R[d * nx + i];
             }
+            if (ROE) {
+                roe(k, l, r, F);
+            } else {
+                double fl[D], fr[D];
+                flux(k, l, fl);
+                flux(k, r, fr);
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                    F[d] = (0.5 * (fl[d] + fr[d])) - (half_alpha * (r[d] - l[d]));
+            }
+#pragma unroll
+            for (int d = 0; d < D; ++d) s_L[d * nx + i] = F[d];
         }
         __syncthreads();
     }
 
     __device__ __forceinline__ double A(const Consts &k, int e) const {
-        const int d = e >= nx ? 1 : 0;
+        const int d = e / nx;
         const int c = e - d * nx;
         const double fm = s_L[d * nx + (c == 0 ? nx - 1 : c - 1)];
         const double neg = -(s_L[e] - fm);
@@ -1129,16 +1279,19 @@ struct SysField {
     }
 
     __device__ void phi(const Consts &k, int rk) {
-        const int tid = threadIdx.x, nt = blockDim.x, n2 = 2 * nx;
-        bad = false;
-        for (int e = tid; e < n2; e += nt) s_u0[e] = cellv(e >= nx, e - (e >= nx) * nx);
+        const int tid = threadIdx.x, nt = blockDim.x, n = D * nx;
+        bad = 0;
+        for (int e = tid; e < n; e += nt) {
+            const int d = e / nx;
+            s_u0[e] = cellv(d, e - d * nx);
+        }
         const int stages = rk == 0 ? 1 : rk;
 #pragma unroll 1
         for (int sg = 0; sg < stages; ++sg) {
             if (sg > 0) __syncthreads();   // committed stage values visible
-            rhs(k, 0);
+            rhs(k);
             const bool last = (sg == stages - 1);
-            for (int e = tid; e < n2; e += nt) {
+            for (int e = tid; e < n; e += nt) {
                 const double a = A(k, e);
                 const double u0 = s_u0[e];
                 double st;
@@ -1147,7 +1300,8 @@ struct SysField {
                 } else if (sg == 0) {
                     st = u0 + k.dt * a;
                 } else {
-                    const double cur = cellv(e >= nx, e - (e >= nx) * nx);
+                    const int d = e / nx;
+                    const double cur = cellv(d, e - d * nx);
                     if (rk == 2) st = ((0.5 * u0) + (0.5 * cur)) + (k.hdt * a);
                     else if (sg == 1) st = ((0.75 * u0) + (0.25 * cur)) + (k.qdt * a);
                     else st = ((u0 / 3.0) + (k.two3 * cur)) + (k.tdt * a);
@@ -1156,27 +1310,28 @@ struct SysField {
                 else put(e, st);
             }
         }
-        if (bad && status) atomicOr(status, MGP_STATUS_NONPOSITIVE_DEPTH);
+        if (bad && status) atomicOr(status, bad);
     }
 };
 
-template <int K, bool ROE>
+template <int K, bool ROE, int D>
 __global__ void __launch_bounds__(256) sys_kernel(const mgp_sweep_args a, const Consts k) {
     extern __shared__ double smem[];
-    SysField<K, ROE> f;
+    SysField<K, ROE, D> f;
     const int nx = (int)a.phi.nx;
     f.nx = nx;
     f.pitch = nx + 2 * K;
+    f.charwise = a.phi.characteristic != 0;
     f.s_u = smem;
-    f.s_u0 = f.s_u + 2 * f.pitch;
-    f.s_L = f.s_u0 + 2 * nx;
-    f.s_R = f.s_L + 2 * nx;
-    double *s_sum = f.s_R + 2 * nx;            // [3 * 32]
+    f.s_u0 = f.s_u + D * f.pitch;
+    f.s_L = f.s_u0 + D * nx;
+    f.s_R = f.s_L + D * nx;
+    double *s_sum = f.s_R + D * nx;            // [3 * 32]
     double *s_psum = s_sum + 3 * 32;           // [3]
     f.s_red = reinterpret_cast<unsigned long long *>(s_psum + 3);
     f.status = a.status;
-    f.bad = false;
-    sweep_body<SysField<K, ROE>, 1>(a, k, f, 2 * nx, 0, 0, s_sum, s_psum, 2 * nx);
+    f.bad = 0;
+    sweep_body<SysField<K, ROE, D>, 1>(a, k, f, D * nx, 0, 0, s_sum, s_psum, D * nx);
 }
 
 __global__ void __launch_bounds__(1024, 1)
@@ -1229,6 +1384,8 @@ Consts make_consts(const mgp_phi &p) {
     k.lf_order = p.lf_order;
     k.m_eff = p.m_eff;
     k.gravity = p.gravity;
+    k.gamma = p.gamma;
+    k.gm1 = p.gamma - 1.0;
     return k;
 }
 
@@ -1432,14 +1589,14 @@ int launch_lf(const mgp_sweep_args &a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
-template <int K, bool ROE>
+template <int K, bool ROE, int D>
 int launch_sys_t(const mgp_sweep_args &a, cudaStream_t st) {
     const int64_t nx = a.phi.nx;
     int nt = (int)((nx + 31) / 32 * 32);
     if (nt > 256) nt = 256;
-    const size_t sm = sizeof(double) * (size_t)(2 * (nx + 2 * K) + 6 * nx + 3 * 32 + 3) +
+    const size_t sm = sizeof(double) * (size_t)(D * (nx + 2 * K) + 3 * D * nx + 3 * 32 + 3) +
                       sizeof(unsigned long long) * 32;
-    auto kern = sys_kernel<K, ROE>;
+    auto kern = sys_kernel<K, ROE, D>;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1454,19 +1611,26 @@ int launch_sys_t(const mgp_sweep_args &a, cudaStream_t st) {
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
 }
 
-template <bool ROE>
-int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
+template <bool ROE, int D>
+int launch_sys_k(const mgp_sweep_args &a, cudaStream_t st) {
     switch (a.phi.weno_k) {
-        case 0: return launch_sys_t<0, ROE>(a, st);
-        case 1: return launch_sys_t<1, ROE>(a, st);
-        case 2: return launch_sys_t<2, ROE>(a, st);
-        case 3: return launch_sys_t<3, ROE>(a, st);
+        case 0: return launch_sys_t<0, ROE, D>(a, st);
+        case 1: return launch_sys_t<1, ROE, D>(a, st);
+        case 2: return launch_sys_t<2, ROE, D>(a, st);
+        case 3: return launch_sys_t<3, ROE, D>(a, st);
     }
     return MGP_EINVAL;
 }
 
+int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
+    const bool roe = a.phi.scheme == MGP_SCHEME_RK_WENO_ROE;
+    if (a.phi.model == MGP_MODEL_EULER)
+        return roe ? launch_sys_k<true, 3>(a, st) : launch_sys_k<false, 3>(a, st);
+    return roe ? launch_sys_k<true, 2>(a, st) : launch_sys_k<false, 2>(a, st);
+}
+
 int64_t max_nx_for(int k, int model) {
-    if (model == MGP_MODEL_SHALLOW_WATER) return kMaxSysNx;
+    if (model == MGP_MODEL_SHALLOW_WATER || model == MGP_MODEL_EULER) return kMaxSysNx;
     return (k == 2 && model == MGP_MODEL_BURGERS) ? 16 * kMaxNx : kMaxNx;
 }
 
@@ -1474,10 +1638,14 @@ int validate(const mgp_sweep_args *a) {
     if (!a) return MGP_EINVAL;
     const mgp_phi &p = a->phi;
     if (p.repeats < 1) return MGP_EINVAL;
-    if (p.model == MGP_MODEL_SHALLOW_WATER) {
+    const bool system = p.model == MGP_MODEL_SHALLOW_WATER || p.model == MGP_MODEL_EULER;
+    if (system) {
         if (p.scheme != MGP_SCHEME_RK_WENO && p.scheme != MGP_SCHEME_RK_WENO_ROE)
             return MGP_EINVAL;
-        if (!(p.gravity > 0.0)) return MGP_EINVAL;   // models.py:139-143
+        if (p.model == MGP_MODEL_SHALLOW_WATER && !(p.gravity > 0.0))
+            return MGP_EINVAL;                        // models.py:139-143
+        if (p.model == MGP_MODEL_EULER && !(p.gamma > 1.0))
+            return MGP_EINVAL;                        // models.py:219-223
     } else if (p.scheme == MGP_SCHEME_RK_WENO_ROE &&
                (p.model != MGP_MODEL_BURGERS || p.nx > kMaxNx)) {
         return MGP_EINVAL;
@@ -1500,14 +1668,13 @@ int validate(const mgp_sweep_args *a) {
         if (a->tail == MGP_TAIL_RESID && (!a->aux || !a->partials)) return MGP_EINVAL;
         return MGP_OK;
     }
-    if (p.model != MGP_MODEL_BURGERS && p.model != MGP_MODEL_ADVECTION &&
-        p.model != MGP_MODEL_SHALLOW_WATER)
+    if (p.model != MGP_MODEL_BURGERS && p.model != MGP_MODEL_ADVECTION && !system)
         return MGP_EINVAL;
     if (p.weno_k < 0 || p.weno_k > 3) return MGP_EINVAL;
     if (p.rk_order < 0 || p.rk_order > 3) return MGP_EINVAL;
     if (p.regime != MGP_SUM_SEQ && p.regime != MGP_SUM_LANE2) return MGP_EINVAL;
     if (p.nx < 2 * p.weno_k + 1 || p.nx > max_nx_for(p.weno_k, p.model)) return MGP_EINVAL;
-    if (p.model != MGP_MODEL_SHALLOW_WATER && p.nx > kMaxNx &&
+    if (!system && p.nx > kMaxNx &&
         p.nx % (((p.nx + kMaxNx - 1) / kMaxNx + 0)) != 0) {
         int cs = 2;
         while (p.nx / cs > kMaxNx || p.nx % cs) {
@@ -1547,9 +1714,8 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (rc != MGP_OK) return rc;
     if (args->n_chunks == 0) return MGP_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    if (args->phi.model == MGP_MODEL_SHALLOW_WATER)
-        return args->phi.scheme == MGP_SCHEME_RK_WENO_ROE ? launch_sys<true>(*args, st)
-                                                          : launch_sys<false>(*args, st);
+    if (args->phi.model == MGP_MODEL_SHALLOW_WATER || args->phi.model == MGP_MODEL_EULER)
+        return launch_sys(*args, st);
     if (args->phi.scheme == MGP_SCHEME_RK_WENO_ROE) return launch_m<kModelBurgersRoe>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(*args, st);
     if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
@@ -1567,7 +1733,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
 
 int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
-int32_t mgp_abi_version(void) { return 2; }
+int32_t mgp_abi_version(void) { return 3; }
 
 int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
     if (k < 0 || k > 3 || !cw16 || !d4 || !sm64) return MGP_EINVAL;

@@ -12,8 +12,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (G_NONE, MODEL_SHALLOW_WATER, MgpPhi, MgpSweepArgs,
-                   STATUS_NONPOSITIVE_DEPTH, SUM_LANE2, SUM_SEQ, TAIL_NONE)
+from ._lib import (G_NONE, MODEL_EULER, MODEL_SHALLOW_WATER, MgpPhi, MgpSweepArgs,
+                   STATUS_NONPOSITIVE_DENSITY, STATUS_NONPOSITIVE_DEPTH,
+                   STATUS_NONPOSITIVE_PRESSURE, STATUS_ROE_NONHYPERBOLIC, SUM_LANE2,
+                   SUM_SEQ, TAIL_NONE)
 from .errors import PhysicalStateError
 
 DTYPE = torch.float64
@@ -95,12 +97,19 @@ def take_status() -> int:
     return v
 
 
+_STATUS_TEXT = (
+    (STATUS_NONPOSITIVE_DEPTH, "non-positive depth (models.py:147-153)"),
+    (STATUS_NONPOSITIVE_DENSITY, "non-positive density (models.py:228-232)"),
+    (STATUS_NONPOSITIVE_PRESSURE, "non-positive pressure (models.py:235-238)"),
+    (STATUS_ROE_NONHYPERBOLIC, "Roe average loses hyperbolicity (models.py:290-293)"),
+)
+
+
 def raise_for_status(v: int) -> None:
-    if v & STATUS_NONPOSITIVE_DEPTH:
-        raise PhysicalStateError("non-positive depth met by the shallow-water "
-                                 "propagator (models.py:147-153)")
     if v:
-        raise PhysicalStateError(f"propagator status {v}")
+        what = [text for bit, text in _STATUS_TEXT if v & bit] or [f"status {v}"]
+        raise PhysicalStateError("inadmissible state met by the system propagator: "
+                                 + "; ".join(what))
 
 
 def check_status() -> None:
@@ -127,7 +136,7 @@ def sweep(phi: MgpPhi, *, n_chunks: int, start, start_stride: int,
           ref=None, ref_cs: int = 0, ref_ss: int = 0, ref_last_next: int = 0,
           count_nonfinite: int = 0, partials=None, status=None,
           what: str = "mgp_sweep"):
-    if status is None and phi.model == MODEL_SHALLOW_WATER:
+    if status is None and phi.model in (MODEL_SHALLOW_WATER, MODEL_EULER):
         status = status_word()
     if _emulator is not None:
         kw = dict(locals())

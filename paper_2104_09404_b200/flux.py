@@ -31,7 +31,7 @@ class WenoConfig:
 
     order: int = 1
     epsilon: float = DEFAULT_EPSILON
-    characteristic: bool = True  # no effect for scalar models (weno.py:222)
+    characteristic: bool = True  # systems: per characteristic field (weno.py:222)
 
     def __post_init__(self):
         if self.order % 2 == 0 or self.degree not in SUPPORTED_DEGREES:
@@ -69,9 +69,9 @@ class SemiDiscreteOperator:
             raise ConfigError(f"{space_grid.n_cells} cells cannot support order "
                               f"{config.weno.order} reconstruction")
         kind = getattr(model, "kind", "")
-        if config.kind == "roe" and kind not in ("burgers", "shallow-water"):
+        if config.kind == "roe" and kind not in ("burgers", "shallow-water", "euler"):
             raise ConfigError(f"the B200 path implements the Roe flux for Burgers and "
-                              f"shallow water, not '{kind}'")
+                              f"the systems, not '{kind}'")
         if not hasattr(model, "abi_model"):
             raise ConfigError(f"model '{getattr(model, 'kind', model)}' is not a "
                               "model of the B200 path")
@@ -89,7 +89,9 @@ class SemiDiscreteOperator:
                       float(dt), float(self.space_grid.dx),
                       float(self.config.weno.epsilon), float(self.model.speed),
                       SCHEME_RK_WENO_ROE if self.config.kind == "roe" else SCHEME_RK_WENO,
-                      0, 0, 1, float(getattr(self.model, "gravity", 0.0)))
+                      0, 0, 1, float(getattr(self.model, "gravity", 0.0)),
+                      float(getattr(self.model, "gamma", 0.0)),
+                      int(bool(self.config.weno.characteristic)), 0)
 
     @property
     def n_components(self) -> int:

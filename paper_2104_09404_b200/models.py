@@ -5,11 +5,13 @@
 BASELINE.json config 1 needs (u_t + a u_x = 0, flux a u, |lambda| = |a|);
 the reference rejects "advection" (tests/test_models.py:197-198), so it is a
 new ``ConservationModel`` subclass with the same shape contract.
-``ShallowWater`` mirrors models.py:136-211 (state (h, hu), gravity g); its
-propagator is the characteristic-WENO system kernel.  The Euler system
-(models.py:214-308) is out of scope: its characteristic projection in the
-reference goes through LAPACK ``np.linalg.inv`` per cell, whose rounding a
-kernel cannot reproduce bit for bit, so ``make_model`` raises ConfigError.
+``ShallowWater`` (models.py:136-211, state (h, hu), gravity g) and ``Euler``
+(models.py:214-308, state (rho, rho u, E), ratio gamma) run on the
+characteristic-WENO system kernel.  Euler's left eigenvectors are the
+inverse of the right ones; the reference takes it with LAPACK
+(``np.linalg.inv``), the kernel with LU + partial pivoting in LAPACK's
+operation order, so Euler results agree with the reference to rounding
+(DESIGN.md "Euler parity"), shallow water bit for bit.
 
 These host methods are the reference's NumPy semantics for callers and
 tests; the device kernels implement the same formulas (csrc/mgrit_phi.cu).
@@ -23,7 +25,9 @@ from .errors import ConfigError, DimensionError, PhysicalStateError
 MODEL_BURGERS = 0         # MGP_MODEL_BURGERS
 MODEL_ADVECTION = 1       # MGP_MODEL_ADVECTION
 MODEL_SHALLOW_WATER = 2   # MGP_MODEL_SHALLOW_WATER
+MODEL_EULER = 3           # MGP_MODEL_EULER
 DEFAULT_GRAVITY = 9.81    # models.py:21
+DEFAULT_GAMMA = 5.0 / 3.0  # models.py:22
 
 
 class ConservationModel:
@@ -136,12 +140,57 @@ class ShallowWater(ConservationModel):
         return np.abs(vel) + np.sqrt(self.gravity * h)
 
 
-_MODEL_KINDS = ("burgers", "advection", "shallow-water")
-_OUT_OF_SCOPE = ("euler",)
+class Euler(ConservationModel):
+    """Ideal-gas Euler system (rho, rho u, E), p = (gamma-1)(E - rho u^2/2)
+    (models.py:214-260)."""
+
+    kind = "euler"
+    n_components = 3
+    abi_model = MODEL_EULER
+    speed = 0.0
+
+    def __init__(self, gamma: float = DEFAULT_GAMMA):
+        if not gamma > 1.0:
+            raise PhysicalStateError(f"gamma must exceed 1, got {gamma}")
+        self.gamma = float(gamma)
+
+    def _primitives(self, u):
+        rho = u[..., 0, :]
+        bad = rho <= 0.0
+        if np.any(bad):
+            raise PhysicalStateError(
+                f"non-positive density in cell {int(np.argmax(bad.reshape(-1)))}")
+        vel = u[..., 1, :] / rho
+        p = (self.gamma - 1.0) * (u[..., 2, :] - 0.5 * rho * vel * vel)
+        bad = p <= 0.0
+        if np.any(bad):
+            raise PhysicalStateError(
+                f"non-positive pressure in cell {int(np.argmax(bad.reshape(-1)))}")
+        return rho, vel, p
+
+    def flux(self, u):
+        self._check_shape(u)
+        rho, vel, p = self._primitives(u)
+        return np.stack([u[..., 1, :], u[..., 1, :] * vel + p, (u[..., 2, :] + p) * vel],
+                        axis=-2)
+
+    def eigenvalues(self, u):
+        self._check_shape(u)
+        rho, vel, p = self._primitives(u)
+        c = np.sqrt(self.gamma * p / rho)
+        return np.stack([vel - c, vel, vel + c], axis=-1)
+
+    def max_abs_speed(self, u):
+        self._check_shape(u)
+        rho, vel, p = self._primitives(u)
+        return np.abs(vel) + np.sqrt(self.gamma * p / rho)
+
+
+_MODEL_KINDS = ("burgers", "advection", "shallow-water", "euler")
 
 
 def make_model(kind: str, *, speed: float = 1.0, gravity: float = DEFAULT_GRAVITY,
-               **_unused) -> ConservationModel:
+               gamma: float = DEFAULT_GAMMA, **_unused) -> ConservationModel:
     """Build a model by name (models.py:318-328 plus "advection")."""
     if kind == "burgers":
         return Burgers()
@@ -149,8 +198,6 @@ def make_model(kind: str, *, speed: float = 1.0, gravity: float = DEFAULT_GRAVIT
         return Advection(speed)
     if kind == "shallow-water":
         return ShallowWater(gravity)
-    if kind in _OUT_OF_SCOPE:
-        raise ConfigError(
-            f"model '{kind}' is outside the B200 path (its characteristic "
-            f"projection uses LAPACK inverses); supported: {_MODEL_KINDS}")
+    if kind == "euler":
+        return Euler(gamma)
     raise ConfigError(f"unknown model '{kind}', expected one of {sorted(_MODEL_KINDS)}")

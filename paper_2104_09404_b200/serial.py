@@ -71,11 +71,18 @@ def solve_serial(stepper, initial_state, time_grid: TemporalGrid,
     if model is not None:
         if getattr(model, "kind", "") == "advection":
             max_speed = abs(model.speed)
-        elif getattr(model, "kind", "") == "shallow-water":
+        elif getattr(model, "kind", "") in ("shallow-water", "euler"):
             # serial.py:47-54: running max over nodes of max |u| + sqrt(g h)
             # (Python max ignores NaN nodes after the first)
-            h, hu = values[:, 0, :], values[:, 1, :]
-            per_node = ((hu / h).abs() + torch.sqrt(model.gravity * h)).amax(dim=1)
+            if model.kind == "shallow-water":
+                h, hu = values[:, 0, :], values[:, 1, :]
+                speed = (hu / h).abs() + torch.sqrt(model.gravity * h)
+            else:
+                rho, mom, en = values[:, 0, :], values[:, 1, :], values[:, 2, :]
+                vel = mom / rho
+                p = (model.gamma - 1.0) * (en - ((0.5 * rho) * vel) * vel)
+                speed = vel.abs() + torch.sqrt((model.gamma * p) / rho)
+            per_node = speed.amax(dim=1)
             per_node = torch.where(torch.isnan(per_node), torch.zeros_like(per_node),
                                    per_node)
             max_speed = float(per_node.max().item())

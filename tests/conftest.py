@@ -55,3 +55,11 @@ def sw_mgrit_golden():
         meta = json.load(f)
     data = np.load(os.path.join(GOLDEN, "sw_mgrit_cases.npz"))
     return {m["name"]: m for m in meta}, data
+
+
+@pytest.fixture(scope="session")
+def euler_golden():
+    with open(os.path.join(GOLDEN, "euler_vectors.json")) as f:
+        index = json.load(f)
+    data = np.load(os.path.join(GOLDEN, "euler_vectors.npz"))
+    return index, data

@@ -580,6 +580,174 @@ def sw_mgrit_cases():
 
 
 # ---------------------------------------------------------------------------
+# Euler (models.py:214-308) and componentwise systems -- SURVEY.md 8(f) rank 4
+#
+# The reference takes Euler's left eigenvectors with np.linalg.inv (LAPACK
+# via OpenBLAS; models.py:270).  inv3_np below restates that inverse as LU
+# with partial pivoting in LAPACK's operation order (the oracle's and the
+# kernel's inv3); running the reference with it substituted pins every other
+# operation of the Euler path bit for bit, and the unmodified reference's
+# outputs give the tolerance check.
+# ---------------------------------------------------------------------------
+
+def inv3_np(m):
+    a = np.array(m, dtype=float, copy=True)
+    shp = a.shape[:-2]
+    perm = np.broadcast_to(np.arange(3), shp + (3,)).copy()
+    with np.errstate(all="ignore"):
+        for j in range(3):
+            pv = j + np.argmax(np.abs(a[..., j:, j]), axis=-1)
+            idx = pv[..., None, None].repeat(3, -1)
+            rj = a[..., j, :].copy()
+            a[..., j, :] = np.take_along_axis(a, idx, axis=-2)[..., 0, :]
+            np.put_along_axis(a, idx, rj[..., None, :], axis=-2)
+            pj = perm[..., j].copy()
+            perm[..., j] = np.take_along_axis(perm, pv[..., None], axis=-1)[..., 0]
+            np.put_along_axis(perm, pv[..., None], pj[..., None], axis=-1)
+            rp = 1.0 / a[..., j, j]
+            for i in range(j + 1, 3):
+                a[..., i, j] = a[..., i, j] * rp
+            for i in range(j + 1, 3):
+                for c in range(j + 1, 3):
+                    a[..., i, c] = a[..., i, c] - a[..., i, j] * a[..., j, c]
+        x = np.empty_like(a)
+        for col in range(3):
+            b = [(perm[..., i] == col).astype(float) for i in range(3)]
+            for kk in range(3):
+                nz = b[kk] != 0
+                for i in range(kk + 1, 3):
+                    b[i] = np.where(nz, b[i] - b[kk] * a[..., i, kk], b[i])
+            for kk in (2, 1, 0):
+                nz = b[kk] != 0
+                b[kk] = np.where(nz, b[kk] / a[..., kk, kk], b[kk])
+                for i in range(kk):
+                    b[i] = np.where(nz, b[i] - b[kk] * a[..., i, kk], b[i])
+            for i in range(3):
+                x[..., i, col] = b[i]
+    return x
+
+
+class lu_inverse:
+    """Context: the reference's np.linalg.inv replaced by inv3_np."""
+
+    def __enter__(self):
+        self.orig = np.linalg.inv
+        np.linalg.inv = inv3_np
+
+    def __exit__(self, *exc):
+        np.linalg.inv = self.orig
+
+
+def eu_fields(rng, shape, kind):
+    nx = shape[-1]
+    x = (np.arange(nx) + 0.5) / nx
+    lead = shape[:-2]
+    u = np.empty(shape)
+    u[..., 0, :] = 1.0 + 0.2 * np.sin(2 * np.pi * x) + 0.05 * rng.random(lead + (nx,))
+    u[..., 1, :] = 0.1 * rng.standard_normal(lead + (nx,))
+    u[..., 2, :] = 2.0 + 0.3 * rng.random(lead + (nx,))
+    if kind == "contact":
+        u[..., 0, :] += np.where(x > 0.5, 0.0, 0.6)
+    elif kind == "nan":
+        u[..., 1, nx // 3] = np.nan
+    elif kind == "vacuum":     # non-positive density -> PhysicalStateError
+        u[..., 0, 5] = -0.1
+    elif kind == "cold":       # non-positive pressure -> PhysicalStateError
+        u[..., 2, 7] = 0.0
+    return np.ascontiguousarray(u)
+
+
+def _ref_call(op, st, rk, u):
+    try:
+        with np.errstate(all="ignore"):
+            return (op.rhs(u) if rk == 0 else st.advance(u)), False
+    except R.PhysicalStateError:
+        return np.full_like(u, np.nan), True
+
+
+def euler_vectors():
+    rng = np.random.default_rng(11)
+    out, index = {}, []
+    nx = 32
+    sg = R.SpatialGrid(1.0, nx)
+    dt = 0.2 * sg.dx
+    n = 0
+    cases = []
+    for flux in ("lf", "roe"):
+        for k in (0, 1, 2, 3):
+            for rk in (0, 1, 2, 3):
+                for shape in ((3, 3, nx), (3, nx)):
+                    kinds = ["smooth", "contact"]
+                    if rk == 3 and len(shape) == 3:
+                        kinds += ["nan", "vacuum", "cold"]
+                    for fk in kinds:
+                        cases.append(("euler", flux, k, rk, shape, fk, True))
+    # componentwise reconstruction (WenoConfig.characteristic = False)
+    for model in ("euler", "shallow-water"):
+        D = 3 if model == "euler" else 2
+        for flux in ("lf", "roe"):
+            for k in (1, 2, 3):
+                for shape in ((3, D, nx), (D, nx)):
+                    cases.append((model, flux, k, 3, shape, "smooth", False))
+    for model, flux, k, rk, shape, fk, charw in cases:
+        m = R.make_model(model)
+        op = R.SemiDiscreteOperator(m, sg, R.FluxConfig(flux, R.WenoConfig(
+            2 * k + 1, characteristic=charw)))
+        st = R.RungeKuttaStepper(op.rhs, dt, max(rk, 1))
+        u = eu_fields(rng, shape, fk) if model == "euler" else sw_fields(rng, shape, fk)
+        y, raised = _ref_call(op, st, rk, u)
+        with lu_inverse():
+            y_lu, raised_lu = _ref_call(op, st, rk, u)
+        assert raised == raised_lu
+        p = oracle.make_params(model=model, k=k, rk_order=rk, dt=dt, dx=sg.dx,
+                               regime=oracle.SUM_LANE2, scheme=3 if flux == "roe" else 0,
+                               characteristic=charw)
+        try:
+            mine = oracle.phi_apply(p, u)
+            assert not raised, (model, flux, k, rk, fk)
+            assert np.array_equal(mine, y_lu, equal_nan=True), (model, flux, k, rk, shape, fk, charw)
+        except oracle.PhysicalStateOracleError:
+            assert raised, (model, flux, k, rk, fk)
+        key = f"eu{n:03d}"
+        out[key + "_in"], out[key + "_out"], out[key + "_out_lu"] = u, y, y_lu
+        index.append(dict(key=key, model=model, flux=flux, k=k, rk=rk, shape=list(shape),
+                          field=fk, characteristic=charw, dt=dt, dx=sg.dx,
+                          gamma=R.make_model("euler").gamma, gravity=9.81, raises=raised))
+        n += 1
+    np.savez_compressed(os.path.join(HERE, "euler_vectors.npz"), **out)
+    with open(os.path.join(HERE, "euler_vectors.json"), "w") as f:
+        json.dump(index, f, indent=0)
+    print(f"euler vectors: {len(index)}")
+
+
+def euler_configs():
+    """high_order_euler_{lf,roe}.cfg: the unmodified reference's tables and
+    the LU-inverse reference's error histories (what a bit-exact Euler path
+    reproduces up to norm summation order)."""
+    out = []
+    for name in ("high_order_euler_lf", "high_order_euler_roe"):
+        cfg = R.load_config(f"/root/reference/pkg/configs/{name}.cfg")
+        res = R.run_sweep(cfg)
+        with lu_inverse():
+            res_lu = R.run_sweep(cfg)
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            R.emit_csv(res.table, os.path.join(d, "t.csv"))
+            text = open(os.path.join(d, "t.csv")).read()
+        fields = {k: (list(v) if isinstance(v, tuple) else v)
+                  for k, v in dataclasses.asdict(cfg).items()}
+        out.append(dict(name=name, config=fields, csv=text, columns=list(res.table.columns),
+                        errors_lu=[list(r.record.errors) for r in res_lu.runs],
+                        level_dts=[list(r.level_dts) for r in res.runs],
+                        level_cfls=[list(r.level_cfls) for r in res.runs],
+                        max_speed=[r.serial.max_speed for r in res.runs],
+                        diverged_at=[r.record.diverged_at for r in res.runs]))
+        print(name, "done")
+    with open(os.path.join(HERE, "euler_configs.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+# ---------------------------------------------------------------------------
 # the checked-in experiment configs through the reference harness
 # (harness.py:369-495) -- SURVEY.md 8(f) rank 3
 # ---------------------------------------------------------------------------
@@ -617,7 +785,10 @@ def config_tables():
 
 if __name__ == "__main__":
     import sys as _sys
-    which = _sys.argv[1:] or ["phi", "mgrit", "lf", "sw", "configs"]
+    which = _sys.argv[1:] or ["phi", "mgrit", "lf", "sw", "euler", "configs"]
+    if "euler" in which:
+        euler_vectors()
+        euler_configs()
     if "configs" in which:
         config_tables()
     if "sw" in which:

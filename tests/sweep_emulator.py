@@ -10,7 +10,7 @@ import torch
 
 import oracle
 
-_MODEL = {0: "burgers", 1: "advection", 2: "shallow-water"}
+_MODEL = {0: "burgers", 1: "advection", 2: "shallow-water", 3: "euler"}
 
 
 def _rows(t, stride, n, nx, off=0):
@@ -22,16 +22,17 @@ def _params(phi, regime):
     return oracle.make_params(model=_MODEL[phi.model], k=phi.weno_k, rk_order=phi.rk_order,
                               dt=phi.dt, dx=phi.dx, eps=phi.epsilon, speed=phi.speed,
                               regime=regime, scheme=phi.scheme, lf_order=phi.lf_order,
-                              m_eff=phi.m_eff, repeats=phi.repeats, gravity=phi.gravity)
+                              m_eff=phi.m_eff, repeats=phi.repeats, gravity=phi.gravity,
+                              gamma=phi.gamma, characteristic=phi.characteristic)
 
 
 def _apply(p, x, n, D, nx, status):
     try:
         return oracle.phi_apply(p, x.reshape(n, D, nx)).reshape(n, D * nx)
-    except oracle.PhysicalStateOracleError:
+    except oracle.PhysicalStateOracleError as e:
         # the kernel flags the status word and completes the sweep
         if status is not None:
-            status.view(-1)[0] |= 1
+            status.view(-1)[0] |= e.bits
         return np.full((n, D * nx), np.nan)
 
 
@@ -47,7 +48,7 @@ def emulate_sweep(phi, *, n_chunks, start, start_stride, n_steps, g_mode, g, g_c
                   store, st_cs, st_ss, tail, tail_regime, tail_g_mode, guess, tail_g, tg_s,
                   tail_out, to_s, tail_out2, to2_s, aux, aux_s, aux2, aux2_s, ref, ref_cs,
                   ref_ss, ref_last_next, count_nonfinite, partials, status, what):
-    D = 2 if phi.model == 2 else 1
+    D = {2: 2, 3: 3}.get(phi.model, 1)
     n, cells = int(n_chunks), int(phi.nx)
     nx = D * cells   # row length
     if n == 0:

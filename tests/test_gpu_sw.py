@@ -84,7 +84,7 @@ def test_sw_rejections():
         P.SemiDiscreteOperator(P.make_model("shallow-water"), sg,
                                P.FluxConfig("lf", P.WenoConfig(5)))
     with pytest.raises(P.ConfigError):
-        P.make_model("euler")
+        P.make_model("navier-stokes")
     with pytest.raises(P.PhysicalStateError):
         P.make_model("shallow-water", gravity=0.0)
 

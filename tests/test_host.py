@@ -17,7 +17,7 @@ def test_config_errors_mirror_reference():
     sg = P.SpatialGrid(1.0, 4)
     with pytest.raises(P.ConfigError):   # 4 cells cannot support WENO5 (flux.py:138-141)
         P.SemiDiscreteOperator(P.make_model("burgers"), sg, P.FluxConfig("lf", P.WenoConfig(5)))
-    with pytest.raises(P.ConfigError):   # Roe: Burgers only (systems out of scope)
+    with pytest.raises(P.ConfigError):   # Roe: Burgers and the systems, not advection
         P.SemiDiscreteOperator(P.make_model("advection"), P.SpatialGrid(1.0, 8),
                                P.FluxConfig("roe", P.WenoConfig(1)))
     with pytest.raises(P.ConfigError):   # matched operators: scalar Burgers only
@@ -25,7 +25,12 @@ def test_config_errors_mirror_reference():
     with pytest.raises(P.ConfigError):
         P.MatchedLFCoarse(P.make_model("burgers"), P.SpatialGrid(1.0, 8), 0.1, 2, 2)
     with pytest.raises(P.ConfigError):
-        P.make_model("euler")
+        P.make_model("navier-stokes")
+    with pytest.raises(P.PhysicalStateError):    # models.py:219-223
+        P.make_model("euler", gamma=1.0)
+    with pytest.raises(P.ConfigError):           # beyond the system kernel's mesh limit
+        P.SemiDiscreteOperator(P.make_model("euler"), P.SpatialGrid(1.0, 4096),
+                               P.FluxConfig("roe", P.WenoConfig(3)))
     op = P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, 8),
                                 P.FluxConfig("lf", P.WenoConfig(3)))
     with pytest.raises(P.ConfigError):
