@@ -79,6 +79,33 @@ __constant__ double c_cw[4][4][4] = MGP_CW_TABLE;
 __constant__ double c_d[4][4] = MGP_D_TABLE;
 __constant__ double c_sm[4][4][4][4] = MGP_SM_TABLE;
 
+// The same tables as compile-time literals for the kernels: after unrolling
+// every index is a constant, so each coefficient becomes an immediate
+// constant of the instruction stream and equal values are shared, instead of
+// one constant-bank load per table entry (the __constant__ copies above stay
+// the single source for host-side checks, mgp_weno_tables).
+#ifndef MGP_CONST_BANK
+__device__ __forceinline__ constexpr double tab_cw(int k, int r, int j) {
+    constexpr double t[4][4][4] = MGP_CW_TABLE;
+    return t[k][r][j];
+}
+__device__ __forceinline__ constexpr double tab_d(int k, int r) {
+    constexpr double t[4][4] = MGP_D_TABLE;
+    return t[k][r];
+}
+__device__ __forceinline__ constexpr double tab_sm(int k, int s, int a, int b) {
+    constexpr double t[4][4][4][4] = MGP_SM_TABLE;
+    return t[k][s][a][b];
+}
+#define CW(k, r, j) tab_cw(k, r, j)
+#define DW(k, r) tab_d(k, r)
+#define SM(k, s, a, b) tab_sm(k, s, a, b)
+#else
+#define CW(k, r, j) c_cw[k][r][j]
+#define DW(k, r) c_d[k][r]
+#define SM(k, s, a, b) c_sm[k][s][a][b]
+#endif
+
 namespace {
 
 using mgp::SharedRcp;
@@ -125,12 +152,25 @@ __device__ __forceinline__ unsigned long long umax64(unsigned long long a,
 
 constexpr unsigned long long kNaNBits = 0x7FF8000000000000ull;
 
+// Warp-wide unsigned 64-bit max (alpha bits of non-negative doubles): the max
+// high word, then the max low word among the lanes holding it -- two REDUX
+// instead of five 64-bit shuffle rounds.
+__device__ __forceinline__ unsigned long long warp_umax64(unsigned long long v) {
+    const unsigned hi = (unsigned)(v >> 32), lo = (unsigned)v;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
 // kernel-internal model id: Burgers with the Roe flux (mgp_phi.scheme ==
 // MGP_SCHEME_RK_WENO_ROE), no global alpha, NaN kept local like the reference
 constexpr int kModelBurgersRoe = 8;
 
 #ifndef MGP_SLIDE_UNROLL
 #define MGP_SLIDE_UNROLL 1
+#endif
+#ifndef MGP_CENTRED_UNROLL
+#define MGP_CENTRED_UNROLL 8
 #endif
 #define MGP_PRAGMA(x) _Pragma(#x)
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
@@ -164,9 +204,9 @@ template <int K, int REG>
 __device__ __forceinline__ double cand_left(const double *win, int r) {
     // left q_r(m): cells m-r+j -> win[K-r+j], window slot K-r+j
     if (REG == MGP_SUM_SEQ || K < 2) {
-        double acc = c_cw[K][r][0] * win[K - r];
+        double acc = CW(K, r, 0) * win[K - r];
 #pragma unroll
-        for (int j = 1; j <= K; ++j) acc = acc + c_cw[K][r][j] * win[K - r + j];
+        for (int j = 1; j <= K; ++j) acc = acc + CW(K, r, j) * win[K - r + j];
         return acc;
     }
     double ev = 0.0, od = 0.0;
@@ -174,7 +214,7 @@ __device__ __forceinline__ double cand_left(const double *win, int r) {
 #pragma unroll
     for (int j = 0; j <= K; ++j) {
         const int slot = K - r + j;
-        const double p = c_cw[K][r][j] * win[K - r + j];
+        const double p = CW(K, r, j) * win[K - r + j];
         if ((slot & 1) == 0) { ev = he ? ev + p : p; he = true; }
         else { od = ho ? od + p : p; ho = true; }
     }
@@ -185,9 +225,9 @@ template <int K, int REG>
 __device__ __forceinline__ double cand_right(const double *win, int r) {
     // right q_r(m-1): cells (m-1)+1+r-j = m+r-j -> win[K+r-j], slot K-r+j
     if (REG == MGP_SUM_SEQ || K < 2) {
-        double acc = c_cw[K][r][0] * win[K + r];
+        double acc = CW(K, r, 0) * win[K + r];
 #pragma unroll
-        for (int j = 1; j <= K; ++j) acc = acc + c_cw[K][r][j] * win[K + r - j];
+        for (int j = 1; j <= K; ++j) acc = acc + CW(K, r, j) * win[K + r - j];
         return acc;
     }
     double ev = 0.0, od = 0.0;
@@ -195,7 +235,7 @@ __device__ __forceinline__ double cand_right(const double *win, int r) {
 #pragma unroll
     for (int j = 0; j <= K; ++j) {
         const int slot = K - r + j;
-        const double p = c_cw[K][r][j] * win[K + r - j];
+        const double p = CW(K, r, j) * win[K + r - j];
         if ((slot & 1) == 0) { ev = he ? ev + p : p; he = true; }
         else { od = ho ? od + p : p; ho = true; }
     }
@@ -214,7 +254,7 @@ __device__ __forceinline__ void beta_block(const double *win, int s, double &fwd
     for (int a = 0; a <= K; ++a)
 #pragma unroll
         for (int b = 0; b <= K; ++b)
-            p[a * (K + 1) + b] = (win[K - s + a] * c_sm[K][s][a][b]) * win[K - s + b];
+            p[a * (K + 1) + b] = (win[K - s + a] * SM(K, s, a, b)) * win[K - s + b];
     if (LEFT) {
         double f = p[0];
 #pragma unroll
@@ -240,7 +280,7 @@ __device__ __forceinline__ double weno_value_ieee(const double *beta, const doub
 #pragma unroll
     for (int r = 0; r <= K; ++r) {
         const double e = eps + beta[r];
-        raw[r] = c_d[K][r] / (e * e);
+        raw[r] = DW(K, r) / (e * e);
     }
     double S = raw[0];
 #pragma unroll
@@ -249,6 +289,24 @@ __device__ __forceinline__ double weno_value_ieee(const double *beta, const doub
 #pragma unroll
     for (int r = 1; r <= K; ++r) v = v + (raw[r] / S) * q[r];
     return v;
+}
+
+// The rare exact path out of line (keeps the hot loop compact in the
+// instruction cache); operands by value so nothing is spilled to call it.
+template <int K>
+__device__ __noinline__ double weno_value_slow_(double b0, double b1, double b2, double b3,
+                                                double q0, double q1, double q2, double q3,
+                                                double eps) {
+    const double beta[4] = {b0, b1, b2, b3};
+    const double q[4] = {q0, q1, q2, q3};
+    return weno_value_ieee<K>(beta, q, eps);
+}
+
+template <int K>
+__device__ __forceinline__ double weno_value_slow(const double *beta, const double *q, double eps) {
+    return weno_value_slow_<K>(beta[0], K >= 1 ? beta[1] : 0.0, K >= 2 ? beta[2] : 0.0,
+                               K >= 3 ? beta[3] : 0.0, q[0], K >= 1 ? q[1] : 0.0,
+                               K >= 2 ? q[2] : 0.0, K >= 3 ? q[3] : 0.0, eps);
 }
 
 template <int K>
@@ -260,7 +318,7 @@ __device__ __forceinline__ double weno_value(const double *beta, const double *q
 #pragma unroll
     for (int r = 0; r <= K; ++r) {
         const double e = eps + beta[r];
-        raw[r] = mgp::div_fast_cnum(c_d[K][r], shared_rcp(e * e), bad);
+        raw[r] = mgp::div_fast_cnum(DW(K, r), shared_rcp(e * e), bad);
     }
     double S = raw[0];
 #pragma unroll
@@ -279,7 +337,49 @@ __device__ __forceinline__ double weno_value(const double *beta, const double *q
 #pragma unroll
             for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(moot_win[t]);
         }
-        if (!moot) v = weno_value_ieee<K>(beta, q, eps);
+        if (!moot) v = weno_value_slow<K>(beta, q, eps);
+    }
+    return v;
+}
+
+// As weno_value, with the validity of all 2K+2 fast-path divisions shown by
+// one range test: if every e_r = eps + beta_r lies in [2^-60, 2^61) then
+// e_r^2 is in [2^-120, 2^122), raw_r = d_r / e_r^2 (d_r >= 1/35) in
+// [2^-128, 2^120), S = sum raw_r in [2^-128, 2^120] and omega_r = raw_r / S
+// in [2^-248, 1] -- every divisor finite, every numerator above 2^-967 and
+// every quotient normal, which is exactly the fast-path predicate of
+// div_shared.cuh.  Otherwise (huge or non-finite fields) the value is
+// recomputed with IEEE `/` unless `moot`.  Two integer operations per e_r
+// replace the per-division checks.
+template <int K>
+__device__ __forceinline__ double weno_value_rc(const double *beta, const double *q, double eps,
+                                                const double *moot_win) {
+    constexpr unsigned kLo = 963u << 20;      // high word of 2^-60
+    constexpr unsigned kSpan = 121u << 20;    // [2^-60, 2^61)
+    double e[K + 1];
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r <= K; ++r) {
+        e[r] = eps + beta[r];
+        ok &= ((unsigned)__double2hiint(e[r]) - kLo) < kSpan;
+    }
+    double raw[K + 1];
+#pragma unroll
+    for (int r = 0; r <= K; ++r) raw[r] = mgp::div_nocheck(DW(K, r), shared_rcp(e[r] * e[r]));
+    double S = raw[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) S = S + raw[r];
+    const SharedRcp R = shared_rcp(S);
+    double v = mgp::div_nocheck(raw[0], R) * q[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) v = v + mgp::div_nocheck(raw[r], R) * q[r];
+    if (!ok) {
+        bool moot = false;
+        if (moot_win) {
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) moot |= !is_finite(moot_win[t]);
+        }
+        if (!moot) v = weno_value_slow<K>(beta, q, eps);
     }
     return v;
 }
@@ -342,7 +442,18 @@ struct Field {
     static constexpr int HALO = H;
     __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
     __device__ __forceinline__ void load(int t, double v) { s_u[sk(t + H)] = v; }
-    __device__ __forceinline__ double result(int t) const { return s_R[sk(t)]; }
+    // centred reconstruction with the merged flux / rhs pass (CS = 1): the
+    // interface states stay readable by neighbouring runs until the stage
+    // ends, so results go to the RK base slots, which only their owner reads
+    static constexpr bool kMerged =
+#ifdef MGP_SLIDING_RECON
+        false;
+#else
+        CS == 1 && P > 0 && K > 0;
+#endif
+    __device__ __forceinline__ double result(int t) const {
+        return kMerged ? s_u0[sk(t)] : s_R[sk(t)];
+    }
     __device__ __forceinline__ void put(int t, double v) {
         s_u[sk(t + H)] = v;
         if (CS == 1) {
@@ -400,6 +511,7 @@ struct Field {
             }
             return m;
         }
+        if (kMerged) return reconstruct_centred(k);
         const int n = (ns - i0 < PC) ? ns - i0 : PC;
         if (n <= 0) return 0;
         if (K == 0) {
@@ -409,8 +521,8 @@ struct Field {
             for (int p = 0; p < n; ++p) {
                 const int i = i0 + p;
                 const double c1 = cell(i + 1);
-                double ul = k.k0_omega * (c_cw[0][0][0] * c0);
-                double ur = k.k0_omega * (c_cw[0][0][0] * c1);
+                double ul = k.k0_omega * (CW(0, 0, 0) * c0);
+                double ur = k.k0_omega * (CW(0, 0, 0) * c1);
                 if (kCheck) {
                     if (!is_finite(c0)) ul = __longlong_as_double(kNaNBits);
                     if (!is_finite(c1)) ur = __longlong_as_double(kNaNBits);
@@ -495,6 +607,61 @@ struct Field {
         return m;
     }
 
+    // Whole-field CTA (CS = 1), P cells per thread: iteration p takes the
+    // window centred on cell c = i0 + 1 + p and produces the two states that
+    // window defines -- the left state of interface c (stored at c mod ns)
+    // and the right state of interface c - 1 -- from one set of beta
+    // products (forward and reverse sums, see beta_block).  The left state of
+    // the thread's first interface i0 is the previous thread's last
+    // iteration, so no window is evaluated twice and nothing is carried
+    // between iterations; the fully unrolled loop keeps the sliding window
+    // in registers without copies.
+    __device__ __forceinline__ unsigned long long reconstruct_centred(const Consts &k) {
+        unsigned long long m = 0;
+        constexpr bool kCheck = (MODEL != MGP_MODEL_BURGERS);
+        constexpr bool burg = (MODEL == MGP_MODEL_BURGERS);
+        const int n = (ns - i0 < PC) ? ns - i0 : PC;
+        if (n <= 0) return 0;
+        double win[2 * K + 1];
+#pragma unroll
+        for (int t = 0; t < 2 * K; ++t) win[t + 1] = cell(i0 + 1 - K + t);
+        MGP_UNROLL(MGP_CENTRED_UNROLL)
+        for (int p = 0; p < PC; ++p) {
+            if (p >= n) break;
+            const int c = i0 + 1 + p;
+#pragma unroll
+            for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
+            win[2 * K] = cell(c + K);
+            bool bad = false;
+            if (kCheck) {
+#pragma unroll
+                for (int t = 0; t <= 2 * K; ++t) bad |= !is_finite(win[t]);
+            }
+            double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
+#pragma unroll
+            for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl[s], br[K - s]);
+#pragma unroll
+            for (int r = 0; r <= K; ++r) {
+                ql[r] = cand_left<K, REG>(win, r);
+                qr[r] = cand_right<K, REG>(win, r);
+            }
+            double ul = weno_value_rc<K>(bl, ql, k.eps, burg ? win : nullptr);
+            double ur = weno_value_rc<K>(br, qr, k.eps, burg ? win : nullptr);
+            if (kCheck && bad) {
+                ul = __longlong_as_double(kNaNBits);
+                ur = ul;
+            }
+            s_L[sk(c == ns ? 0 : c)] = ul;
+            s_R[sk(c - 1)] = ur;
+            if (burg) {
+                m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
+                // a non-finite cell makes the reference's alpha NaN
+                if (!is_finite(win[K])) m = kNaNBits;
+            }
+        }
+        return m;
+    }
+
     // A = SemiDiscreteOperator.rhs(s_u) for the owned cells (flux.py:70-88,
     // 159-161).  Precondition: s_u complete (caller synchronised).  On
     // return A[] holds the owned cells' rhs; s_u is unchanged.
@@ -534,9 +701,7 @@ struct Field {
         trace(2);
         double half_alpha;
         if (MODEL == MGP_MODEL_BURGERS) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                m = umax64(m, __shfl_xor_sync(0xffffffffu, m, o));
+            m = warp_umax64(m);
             const int tid = threadIdx.x;
             if ((tid & 31) == 0) s_red[tid >> 5] = m;
             __syncthreads();
@@ -557,9 +722,33 @@ struct Field {
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         } else {
             half_alpha = k.half_alpha_adv;
+            // CS = 1: the left state of each run's first interface was
+            // written by the previous thread (reconstruct_centred)
             if (CS > 1) sync();
+            else if (P > 0 && K > 0) __syncthreads();
         }
         trace(3);
+        if (kMerged) {
+            // each thread forms the flux of the interface left of its run
+            // itself (one extra flux per run) instead of a flux pass, a
+            // barrier and a re-read
+            if (i0 < ns) {
+                const int il = (i0 == 0) ? ns - 1 : i0 - 1;
+                double fm = lf(k, s_L[sk(il)], s_R[sk(il)], half_alpha);
+#pragma unroll
+                for (int p = 0; p < PC; ++p) {
+                    const int c = i0 + p;
+                    if (c < ns) {
+                        const double f = lf(k, s_L[sk(c)], s_R[sk(c)], half_alpha);
+                        const double neg = -(f - fm);
+                        A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+                        fm = f;
+                    }
+                }
+            }
+            trace(4);
+            return;
+        }
 #pragma unroll
         for (int p = 0; p < PC; ++p) {
             const int i = i0 + p;
@@ -637,7 +826,7 @@ struct Field {
     __device__ __forceinline__ void store_res(const double *v) {
 #pragma unroll
         for (int p = 0; p < PC; ++p)
-            if (i0 + p < ns) s_R[sk(i0 + p)] = v[p];
+            if (i0 + p < ns) (kMerged ? s_u0 : s_R)[sk(i0 + p)] = v[p];
     }
 };
 
@@ -1518,6 +1707,18 @@ int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
 template <int K, int REG, int MODEL>
 int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
     const int cs = cluster_size(a);
+#ifdef MGP_QUICK
+    if (cs > 1) return MGP_EINVAL;
+    if constexpr (K != 2) {
+        return MGP_EINVAL;
+    } else {
+        switch (run_length(a.phi.nx, a.n_chunks)) {
+            case 4: return launch_r<K, REG, MODEL, 4>(a, st);
+            case 8: return launch_r<K, REG, MODEL, 8>(a, st);
+        }
+        return MGP_EINVAL;
+    }
+#else
     if (cs > 1) {
       if constexpr (K != 2 || MODEL != MGP_MODEL_BURGERS) {
         return MGP_EINVAL;
@@ -1550,6 +1751,7 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
         case 8: return launch_r<K, REG, MODEL, 8>(a, st);
     }
     return MGP_EINVAL;
+#endif
 }
 
 template <int MODEL>
@@ -1714,6 +1916,12 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (rc != MGP_OK) return rc;
     if (args->n_chunks == 0) return MGP_OK;
     cudaStream_t st = (cudaStream_t)stream;
+#ifdef MGP_QUICK
+    // experiment builds (tools/): Burgers RK-WENO with the global LF flux only
+    if (args->phi.model != MGP_MODEL_BURGERS || args->phi.scheme != MGP_SCHEME_RK_WENO)
+        return MGP_EINVAL;
+    return launch_m<MGP_MODEL_BURGERS>(*args, st);
+#else
     if (args->phi.model == MGP_MODEL_SHALLOW_WATER || args->phi.model == MGP_MODEL_EULER)
         return launch_sys(*args, st);
     if (args->phi.scheme == MGP_SCHEME_RK_WENO_ROE) return launch_m<kModelBurgersRoe>(*args, st);
@@ -1721,6 +1929,7 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
     if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
     if (args->phi.model == MGP_MODEL_BURGERS) return launch_m<MGP_MODEL_BURGERS>(*args, st);
     return launch_m<MGP_MODEL_ADVECTION>(*args, st);
+#endif
 }
 
 int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *out,

@@ -44,6 +44,8 @@ for name in sys.argv[1:] or ["c2", "c3"]:
     pts = m * nc * nx
     res[name + "_fused_fc_ms"] = ms
     res[name + "_fused_fc_gpts"] = pts / ms / 1e6
+    if os.environ.get("MGP_KT_NOMARCH"):
+        continue
     # sequential march: n steps of the finest propagator from u0 (finite)
     n = min(1024, pb.n_t)
     traj = torch.empty(n + 1, nx, dtype=torch.float64, device="cuda")
