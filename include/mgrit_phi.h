@@ -18,6 +18,10 @@
  *                         MgritHierarchy.residual_norm mgrit.py:264-270
  *                         rel_l2_spacetime_error      grid.py:96-108
  *                         solve_serial                serial.py:40-61
+ *   mgp_relax_fcf    -- MgritHierarchy.relax(0) (mgrit.py:193-197) of the
+ *                       C-points-only finest level as one launch, optionally
+ *                       with fine_values() (mgrit.py:272-273) of the relaxed
+ *                       iterate fused in
  *   mgp_sum_partials -- deterministic reduction of the per-chunk partial sums
  *                       the sweep writes (residual^2, error^2, non-finite
  *                       count), replacing np.linalg.norm (mgrit.py:270,
@@ -180,6 +184,57 @@ typedef struct mgp_sweep_args {
 
 int mgp_sweep(const mgp_sweep_args *args, void *stream);
 
+/*
+ * mgp_relax_fcf: the finest level's relaxation over C-points only, as ONE
+ * launch (MgritHierarchy.relax(0), mgrit.py:193-197, with the F-points
+ * implicit -- c_relax after the F-relaxation they derive from):
+ *
+ *   for every CF-interval j in [0, n_chunks):
+ *       x = cs[j*cs_s];  m-1 times x = Phi(x) (+ 0.0 per g_mode)   (F)
+ *       x = Phi(x) (+ 0.0);  cd[(j+1)*cd_s] = x                     (C)
+ *   and, when fstore != NULL, the final F-relaxation of the relaxed iterate:
+ *       for every interval i: x = (i == 0 ? c0 : new C-point i);
+ *       for s = 1..m-1: x = Phi(x) (+ 0.0); fstore[i*f_cs + (s-1)*f_ss] = x
+ *   where c0 = f0_start if non-NULL (the new C-point 0 of a call that
+ *   continues an earlier one, e.g. a later piece of a pipelined relaxation),
+ *   else cs[0], which is then also copied to cd[0] (node 0 is kept).
+ *   cstore (optional) receives every C-point of the relaxed iterate, rows
+ *   0..n_chunks at cstore[i*cst_s] (e.g. the C-point rows of a trajectory
+ *   buffer whose F-point rows are fstore).
+ *
+ * i.e. exactly mgp_sweep(n_steps = m-1, TAIL_PHI) followed by
+ * mgp_sweep(n_steps = m-1, store) on the new C-points, bit for bit.  Each
+ * interval's C-step runs straight into the next interval's final F-steps
+ * (one chain of 2m-1 steps), and single steps of the chains are handed to
+ * persistent CTAs (one per resident slot) from a ticket counter; between
+ * steps the field travels through an L2-resident ring in `workspace`, so
+ * every slot stays busy to the end of the launch.  cd must not alias cs.
+ * workspace: at least mgp_relax_fcf_workspace() bytes, zero-filled once
+ * before first use (every call leaves it clean again, so CUDA graph replays
+ * work; calls sharing a workspace must be stream-ordered); epoch: non-zero
+ * (reserved).  Scalar Burgers RK-WENO fields of nx <= 4096 (one CTA per
+ * field) in the batched sum regime; anything else returns MGP_EINVAL and
+ * the caller uses the two mgp_sweep launches.
+ */
+typedef struct mgp_fcf_args {
+    mgp_phi phi;
+    int64_t n_chunks;     /* CF-intervals (N_t / m)                  */
+    int32_t m;            /* coarsening factor >= 1                   */
+    int32_t g_mode;       /* MGP_G_NONE or MGP_G_ZERO                 */
+    const double *cs;     int64_t cs_s;
+    double *cd;           int64_t cd_s;
+    double *fstore;       int64_t f_cs, f_ss;
+    double *cstore;       int64_t cst_s;
+    const double *f0_start;
+    void *workspace;      int64_t workspace_bytes;
+    uint32_t epoch;
+    int32_t segment;      /* steps per hand-over segment of the chains taken
+                             last (0 = whole chains, the measured default) */
+} mgp_fcf_args;
+int mgp_relax_fcf(const mgp_fcf_args *args, void *stream);
+/* Workspace bytes mgp_relax_fcf needs for this propagator and interval
+ * count on the current device (0 if the fused path does not apply). */
+int64_t mgp_relax_fcf_workspace(const mgp_phi *phi, int64_t n_chunks, int32_t m);
 /* out[j] = sum_b partials[width*b + j] for j < width (width <= 4), summed in a
  * fixed order independent of launch timing (deterministic). */
 int mgp_sum_partials(const double *partials, int64_t n, int32_t width,

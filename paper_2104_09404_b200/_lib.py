@@ -32,7 +32,7 @@ STATUS_NONPOSITIVE_DEPTH = 1
 STATUS_NONPOSITIVE_DENSITY = 2
 STATUS_NONPOSITIVE_PRESSURE = 4
 STATUS_ROE_NONHYPERBOLIC = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -84,9 +84,25 @@ class MgpSweepArgs(ctypes.Structure):
     ]
 
 
+class MgpFcfArgs(ctypes.Structure):
+    _fields_ = [
+        ("phi", MgpPhi),
+        ("n_chunks", _I64),
+        ("m", _I32), ("g_mode", _I32),
+        ("cs", _P), ("cs_s", _I64),
+        ("cd", _P), ("cd_s", _I64),
+        ("fstore", _P), ("f_cs", _I64), ("f_ss", _I64),
+        ("cstore", _P), ("cst_s", _I64),
+        ("f0_start", _P),
+        ("workspace", _P), ("workspace_bytes", _I64),
+        ("epoch", ctypes.c_uint32), ("segment", _I32),
+    ]
+
+
 EXPORTED_SYMBOLS = ("mgp_sweep", "mgp_sum_partials", "mgp_max_nx",
                     "mgp_abi_version", "mgp_weno_tables", "mgp_launch_count",
-                    "mgp_sweep_args_layout")
+                    "mgp_sweep_args_layout", "mgp_relax_fcf",
+                    "mgp_relax_fcf_workspace")
 
 
 def build(verbose: bool = False) -> str:
@@ -126,6 +142,10 @@ def load():
     lib.mgp_launch_count.restype = _I64
     lib.mgp_sweep_args_layout.argtypes = [ctypes.POINTER(_I64), _I32]
     lib.mgp_sweep_args_layout.restype = _I32
+    lib.mgp_relax_fcf.argtypes = [ctypes.POINTER(MgpFcfArgs), _P]
+    lib.mgp_relax_fcf.restype = ctypes.c_int
+    lib.mgp_relax_fcf_workspace.argtypes = [ctypes.POINTER(MgpPhi), _I64, _I32]
+    lib.mgp_relax_fcf_workspace.restype = _I64
     _lib = lib
     return lib
 

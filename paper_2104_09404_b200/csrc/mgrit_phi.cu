@@ -15,6 +15,7 @@
 //   models.py:107-117 Burgers flux / speed
 //   stepper.py:50-62 SSP-RK1/2/3;  mgrit.py:168-270 level operations.
 #include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stddef.h>
@@ -117,6 +118,9 @@ constexpr int kMaxRun = 8;
 constexpr int64_t kMaxNx = (int64_t)kMaxThreads * kMaxRun;
 
 unsigned long long g_launches = 0;
+#ifdef MGP_FCF_TRACE
+__device__ unsigned long long g_fcf_trace[4 * 8192];
+#endif
 
 #ifdef MGP_TRACE
 __device__ long long g_trace[8192];
@@ -1013,6 +1017,211 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
 }
 
 // ---------------------------------------------------------------------------
+// Fused FCF relaxation of the finest level (mgp_relax_fcf, include/
+// mgrit_phi.h).  Chain j (j < nc) = interval j's m-1 F-steps, its C-step
+// (new C-point j+1) and, with F-point storage, interval j+1's m-1 final
+// F-steps; chain nc = interval 0's final F-steps.  Persistent CTAs (one per
+// resident slot) take work from a ticket counter: first whole chains, then
+// the last R <= G chains cut into segments of S steps, segment-major, so
+// the work still handed out at the end is short and a segment's
+// predecessor (the same chain's previous segment) was taken about R
+// tickets earlier; the field travels between segments through an
+// L2-resident row per split chain.  Dynamic assignment keeps every slot busy
+// to the end: co-resident CTAs do not progress at equal rates (the warp
+// scheduler favours older warps; measured up to 1.4x on B200), which a
+// static split of the steps turns into an idle tail, and hand-overs cost
+// about a tenth of a step each (exposed L2 latency), hence whole chains
+// wherever the tail allows.
+// ---------------------------------------------------------------------------
+struct FcfPlan {
+    int64_t nc, nchains, W;   // intervals, chains (+1 with F-point storage), tickets
+    int64_t K, R;             // chains taken whole; the last R = nchains - K are split
+    int64_t Gmax;             // resident CTA slots (workspace layout)
+    int m, L, S;              // coarsening factor, regular chain length, segment steps
+    bool fstore;
+    __host__ __device__ int len(int64_t j) const {
+        if (!fstore) return m;
+        if (j < nc - 1) return L;
+        return j == nc - 1 ? m : m - 1;
+    }
+    __host__ __device__ int nseg(int n) const { return (n + S - 1) / S; }
+    // split chains with more than t segments (lengths never increase with j)
+    __host__ __device__ int64_t count(int t) const {
+        int64_t c = R;
+        if (fstore) {
+            if (nc - 1 >= K && nseg(m) <= t) --c;
+            if (nc >= K && nseg(m - 1) <= t) --c;
+        }
+        return c;
+    }
+    __host__ __device__ int64_t n_units() const {
+        int64_t w = K;
+        for (int t = 0; t < nseg(L); ++t) w += count(t);
+        return w;
+    }
+    // ticket i -> chain j and segment t (steps [t S, min((t+1) S, len(j)))),
+    // t = -1 for a chain taken whole
+    __host__ __device__ void unit(int64_t i, int64_t &j, int &t) const {
+        if (i < K) {
+            j = i;
+            t = -1;
+            return;
+        }
+        i -= K;
+        for (int u = 0; u < nseg(L); ++u) {
+            const int64_t c = count(u);
+            if (i < c) {
+                j = K + i;
+                t = u;
+                return;
+            }
+            i -= c;
+        }
+        j = -1;
+        t = 0;
+    }
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// ring-row tag: chain j has completed s steps (0 = row never used)
+__device__ __forceinline__ unsigned long long fcf_tag(int64_t j, int s) {
+    return ((unsigned long long)(j + 1) << 20) | (unsigned)s;
+}
+
+template <class F>
+__device__ __forceinline__ void fcf_load(F &f, const double *x0, int ns, bool coherent) {
+    for (int t = (int)threadIdx.x - F::HALO; t < ns + F::HALO; t += blockDim.x) {
+        int c = t < 0 ? t + ns : (t >= ns ? t - ns : t);
+        f.load(t, coherent ? __ldcg(x0 + c) : x0[c]);
+    }
+}
+
+template <int K, int REG, int MODEL, int P, int REGS>
+__global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts k,
+                                             const FcfPlan pl) {
+    extern __shared__ double smem[];
+    __shared__ long long s_ticket;
+    using F = Field<K, REG, MODEL, P, 1>;
+    F f;
+    const int ns = (int)a.phi.nx;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    f.ns = ns;
+    f.q = 0;
+    f.run = tid;
+    f.i0 = tid * F::PC;
+    f.s_u = smem;
+    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
+    f.s_R = f.s_L + sk_size(ns);
+    f.s_u0 = f.s_R + sk_size(ns);
+    f.s_red = reinterpret_cast<unsigned long long *>(f.s_u0 + sk_size(ns));
+    // workspace (layout fixed per device and mesh, whatever the call's
+    // interval count): ticket and exit counters | Gmax tags | Gmax rows
+    unsigned long long *ctr = static_cast<unsigned long long *>(a.workspace);
+    unsigned long long *tags = ctr + 2;
+    double *ring = reinterpret_cast<double *>(tags + pl.Gmax);
+    const double *c0 = a.f0_start ? a.f0_start : a.cs;   // new C-point 0
+    const int m = pl.m;
+    if (blockIdx.x == 0) {
+        for (int c = tid; c < ns; c += nt) {
+            const double v = c0[c];
+            if (!a.f0_start) a.cd[c] = v;
+            if (a.cstore) a.cstore[c] = v;
+        }
+    }
+    for (;;) {
+        if (tid == 0) s_ticket = (long long)atomicAdd(ctr, 1ull);
+        __syncthreads();   // also: the previous unit's stores to s_u are done
+        const int64_t i = s_ticket;
+        if (i >= pl.W) break;
+#ifdef MGP_FCF_TRACE
+        unsigned long long t_unit0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_unit0));
+#endif
+        int64_t j;
+        int seg;
+        pl.unit(i, j, seg);
+        const int len = pl.len(j);
+        const int s0 = seg < 0 ? 0 : seg * pl.S;
+        const int s1 = (seg < 0 || s0 + pl.S >= len) ? len : s0 + pl.S;
+        const int64_t row = j - pl.K;               // split chains only
+        double *rrow = ring + (row < 0 ? 0 : row) * ns;
+        if (s0 > 0) {
+            // a later segment needs the chain's previous one (taken about R
+            // tickets earlier, normally long done)
+            if (tid == 0)
+                while (ld_acquire_u64(tags + row) != fcf_tag(j, s0)) __nanosleep(32);
+            __syncthreads();
+        }
+        if (s0 == 0) fcf_load(f, j == pl.nc ? c0 : a.cs + j * a.cs_s, ns, false);
+        else fcf_load(f, rrow, ns, true);
+        for (int st = s0; st < s1; ++st) {
+            f.sync();
+            f.phi(k, a.phi.rk_order);
+            __syncthreads();
+            for (int rep = 1; rep < a.phi.repeats; ++rep) {   // ComposedStepper
+                for (int c = tid; c < ns; c += nt) f.put(c, f.result(c));
+                f.sync();
+                f.phi(k, a.phi.rk_order);
+                __syncthreads();
+            }
+            // where this step's state goes
+            double *dst = nullptr, *dst2 = nullptr;
+            if (j == pl.nc) {                       // interval 0's final F-steps
+                dst = a.fstore + (int64_t)st * a.f_ss;
+            } else if (st == m - 1) {               // C-step: new C-point j+1
+                dst = a.cd + (j + 1) * a.cd_s;
+                if (a.cstore) dst2 = a.cstore + (j + 1) * a.cst_s;
+            } else if (st >= m) {                   // interval j+1's final F-steps
+                dst = a.fstore + (j + 1) * a.f_cs + (int64_t)(st - m) * a.f_ss;
+            }
+            const bool hand = (st == s1 - 1) && (s1 < len);   // hand the field on
+            for (int c = tid; c < ns; c += nt) {
+                const double v = add_g(f.result(c), a.g_mode, nullptr, c);
+                f.put(c, v);
+                if (dst) dst[c] = v;
+                if (dst2) dst2[c] = v;
+                if (hand) __stcg(rrow + c, v);
+            }
+        }
+        if (s1 < len) {
+            __threadfence();   // every thread's row stores before the release
+            __syncthreads();
+            if (tid == 0) st_release_u64(tags + row, fcf_tag(j, s1));
+        }
+#ifdef MGP_FCF_TRACE
+        if (tid == 0 && i < 8192) {
+            unsigned long long t1;
+            unsigned smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_fcf_trace[4 * i] = t_unit0;
+            g_fcf_trace[4 * i + 1] = t1;
+            g_fcf_trace[4 * i + 2] = blockIdx.x;
+            g_fcf_trace[4 * i + 3] = smid | ((unsigned long long)(s1 - s0) << 32);
+        }
+#endif
+    }
+    // the last CTA out leaves the workspace clean for the next call
+    if (tid == 0) {
+        __threadfence();
+        const unsigned long long done = atomicAdd(ctr + 1, 1ull);
+        if (done == (unsigned long long)gridDim.x - 1) {
+            for (int64_t r = 0; r < pl.R; ++r) tags[r] = 0ull;
+            ctr[0] = 0ull;
+            ctr[1] = 0ull;
+            __threadfence();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // One-step Lax-Friedrichs family (stepper.py:85-167), Burgers only:
 //   E(u)_i = 0.5 (u_{i+1} + u_{i-1}),  D(f)_i = (f_{i+1} - f_{i-1}) / (2 dx)
 //   one-step (matched-lf-fine, rediscretized-lf):  Phi(u) = E u - dt D f(u)
@@ -1831,6 +2040,102 @@ int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
     return roe ? launch_sys_k<true, 2>(a, st) : launch_sys_k<false, 2>(a, st);
 }
 
+// --- fused FCF relaxation (mgp_relax_fcf) ----------------------------------
+struct FcfLaunch {
+    int G = 0, nt = 0;
+    size_t smem = 0;
+    int64_t R = 0, Gmax = 0, bytes = 0;
+};
+
+template <int K, int P>
+int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
+    auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>;
+    const int ns = (int)phi.nx;
+    L.nt = threads_for(ns, P);
+    L.smem = smem_bytes(ns, K, 1);
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024) != cudaSuccess)
+            return MGP_ECUDA;
+        attr_set = true;
+    }
+    int dev = 0, nsm = 0, per = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, L.nt, L.smem) != cudaSuccess)
+        return MGP_ECUDA;
+    // one CTA per resident slot, at most one per chain; with more chains
+    // than CTAs the last G chains are split
+    const int64_t nchains = nc + (fstore ? 1 : 0);
+    L.Gmax = (int64_t)per * nsm;
+    int64_t G = L.Gmax;
+    if (G > nchains) G = nchains;
+    if (G < 1) return MGP_EINVAL;
+    L.G = (int)G;
+    L.R = nchains > G ? G : 0;
+    L.bytes = (2 + L.Gmax) * 8 + L.Gmax * ns * (int64_t)sizeof(double);
+    return MGP_OK;
+}
+
+template <int K, int P>
+int fcf_launch(const mgp_fcf_args &a, cudaStream_t st) {
+    FcfLaunch L;
+    const bool fstore = a.fstore != nullptr;
+    const int rc = fcf_setup<K, P>(a.phi, a.n_chunks, fstore, L);
+    if (rc != MGP_OK) return rc;
+    if (a.workspace_bytes < L.bytes) return MGP_EINVAL;
+    FcfPlan pl;
+    pl.nc = a.n_chunks;
+    pl.m = a.m;
+    pl.fstore = fstore;
+    pl.nchains = a.n_chunks + (fstore ? 1 : 0);
+    pl.L = fstore ? 2 * a.m - 1 : a.m;
+    pl.R = L.R;
+    pl.Gmax = L.Gmax;
+    pl.K = pl.nchains - L.R;
+    // segment length of the chains taken last; measured on B200 for C2
+    // shapes: whole chains (S = L) and S = 1, 2 within 1-2 %
+    pl.S = (a.segment > 0 && a.segment < pl.L) ? a.segment : pl.L;
+    pl.W = pl.n_units();
+    fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>
+        <<<L.G, L.nt, L.smem, st>>>(a, make_consts(a.phi), pl);
+    ++g_launches;
+    return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
+}
+
+// the fused path covers scalar Burgers RK-WENO fields of one CTA in the
+// batched (sequential-sum) regime; MGP_EINVAL otherwise
+bool fcf_supported(const mgp_phi &p, int64_t nc) {
+    return p.model == MGP_MODEL_BURGERS && p.scheme == MGP_SCHEME_RK_WENO &&
+           p.regime == MGP_SUM_SEQ && p.weno_k >= 0 && p.weno_k <= 3 &&
+           p.rk_order >= 0 && p.rk_order <= 3 && p.repeats >= 1 &&
+           p.nx >= 2 * p.weno_k + 1 && p.nx <= kMaxNx && p.dx > 0.0 && p.epsilon > 0.0 &&
+           nc >= 1;
+}
+
+template <class Fn>
+int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
+    const int run = run_length(p.nx, nc > 1 ? nc : 2);
+    switch (p.weno_k) {
+#define MGP_FCF_K(KK)                                                   \
+    case KK:                                                            \
+        if (run == 4) return fn(std::integral_constant<int, KK>{},      \
+                                std::integral_constant<int, 4>{});      \
+        if (run == 8) return fn(std::integral_constant<int, KK>{},      \
+                                std::integral_constant<int, 8>{});      \
+        return MGP_EINVAL;
+#ifndef MGP_QUICK
+        MGP_FCF_K(0)
+        MGP_FCF_K(1)
+        MGP_FCF_K(3)
+#endif
+        MGP_FCF_K(2)
+#undef MGP_FCF_K
+    }
+    return MGP_EINVAL;
+}
+
 int64_t max_nx_for(int k, int model) {
     if (model == MGP_MODEL_SHALLOW_WATER || model == MGP_MODEL_EULER) return kMaxSysNx;
     return (k == 2 && model == MGP_MODEL_BURGERS) ? 16 * kMaxNx : kMaxNx;
@@ -1932,6 +2237,38 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
 #endif
 }
 
+int mgp_relax_fcf(const mgp_fcf_args *args, void *stream) {
+    if (!args) return MGP_EINVAL;
+    const mgp_fcf_args &a = *args;
+    if (!fcf_supported(a.phi, a.n_chunks) || a.m < 1 || !a.cs || !a.cd || !a.workspace ||
+        a.segment < 0 ||
+        a.epoch == 0 || (a.g_mode != MGP_G_NONE && a.g_mode != MGP_G_ZERO))
+        return MGP_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    return fcf_dispatch(a.phi, a.n_chunks, [&](auto kk, auto pp) {
+        return fcf_launch<decltype(kk)::value, decltype(pp)::value>(a, st);
+    });
+}
+
+#ifdef MGP_FCF_TRACE
+int mgp_debug_fcf_trace(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_fcf_trace, sizeof(unsigned long long) * 4 * 8192) ==
+                   cudaSuccess ? 0 : 2;
+}
+#endif
+
+int64_t mgp_relax_fcf_workspace(const mgp_phi *phi, int64_t n_chunks, int32_t m) {
+    if (!phi || m < 1 || !fcf_supported(*phi, n_chunks)) return 0;
+    int64_t bytes = 0;
+    const int rc = fcf_dispatch(*phi, n_chunks, [&](auto kk, auto pp) {
+        FcfLaunch L;   // with F-point storage (the larger of the two plans)
+        const int r = fcf_setup<decltype(kk)::value, decltype(pp)::value>(*phi, n_chunks, true, L);
+        bytes = L.bytes;
+        return r;
+    });
+    return rc == MGP_OK ? bytes : 0;
+}
+
 int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *out,
                      void *stream) {
     if (!partials || !out || n < 0 || width < 1 || width > 4) return MGP_EINVAL;
@@ -1942,7 +2279,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
 
 int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
-int32_t mgp_abi_version(void) { return 3; }
+int32_t mgp_abi_version(void) { return 4; }
 
 int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
     if (k < 0 || k > 3 || !cw16 || !d4 || !sm64) return MGP_EINVAL;

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (G_NONE, MODEL_EULER, MODEL_SHALLOW_WATER, MgpPhi, MgpSweepArgs,
+from ._lib import (G_NONE, MODEL_EULER, MODEL_SHALLOW_WATER, MgpFcfArgs, MgpPhi, MgpSweepArgs,
                    STATUS_NONPOSITIVE_DENSITY, STATUS_NONPOSITIVE_DEPTH,
                    STATUS_NONPOSITIVE_PRESSURE, STATUS_ROE_NONHYPERBOLIC, SUM_LANE2,
                    SUM_SEQ, TAIL_NONE)
@@ -171,3 +171,34 @@ def sum_partials(partials: torch.Tensor, n: int, width: int, out: torch.Tensor):
     rc = _lib.load().mgp_sum_partials(ptr(partials), int(n), int(width), ptr(out),
                                       ctypes.c_void_p(stream_handle()))
     _lib.check(rc, "mgp_sum_partials")
+
+
+def fcf_workspace_bytes(phi: MgpPhi, n_chunks: int, m: int) -> int:
+    """Workspace the fused FCF relaxation needs (0: not available for this
+    propagator / interval count -- the caller then issues the two sweeps)."""
+    if _emulator is not None:
+        return 0
+    return int(_lib.load().mgp_relax_fcf_workspace(ctypes.byref(phi), int(n_chunks), int(m)))
+
+
+def relax_fcf(phi: MgpPhi, *, n_chunks: int, m: int, g_mode: int, cs, cd, workspace,
+              fstore=None, f_cs: int = 0, f_ss: int = 0, cstore=None, cst_s: int = 0,
+              f0_start=None, cs_s: int | None = None, cd_s: int | None = None,
+              segment: int = 0, what: str = "mgp_relax_fcf"):
+    """One fused launch of the finest level's FCF relaxation (mgp_relax_fcf,
+    include/mgrit_phi.h): new C-points into ``cd`` and, with ``fstore``, the
+    relaxed iterate's F-points."""
+    a = MgpFcfArgs()
+    a.phi = phi
+    a.n_chunks, a.m, a.g_mode = int(n_chunks), int(m), int(g_mode)
+    nx = int(phi.nx)
+    a.cs, a.cs_s = ptr(cs), int(nx if cs_s is None else cs_s)
+    a.cd, a.cd_s = ptr(cd), int(nx if cd_s is None else cd_s)
+    a.fstore, a.f_cs, a.f_ss = ptr(fstore), int(f_cs), int(f_ss)
+    a.cstore, a.cst_s = ptr(cstore), int(cst_s)
+    a.f0_start = ptr(f0_start)
+    a.workspace, a.workspace_bytes = ptr(workspace), int(workspace.numel())
+    a.epoch = 1    # the kernel leaves its hand-over flags cleared
+    a.segment = int(segment)
+    rc = _lib.load().mgp_relax_fcf(ctypes.byref(a), ctypes.c_void_p(stream_handle()))
+    _lib.check(rc, what)

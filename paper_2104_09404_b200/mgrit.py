@@ -209,6 +209,8 @@ class MgritHierarchy:
         self._u = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
         self._g = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
         self._phi_buf = torch.empty(max(n1, 1), nx, **kw)
+        # fused FCF relaxation: steps per hand-over segment (0 = whole chains)
+        self._fcf_segment = 0
         self._partials = torch.empty(max(self.n[0] + 1, 1) * 3, **kw)
         self._sums = torch.empty(4, **kw)
 
@@ -221,6 +223,21 @@ class MgritHierarchy:
         if self._c[1 - i] is None:
             self._c[1 - i] = torch.empty_like(self._c[i])
         return 1 - i
+
+    def _fcf_workspace(self):
+        """Workspace of the fused finest-level FCF relaxation (mgp_relax_fcf),
+        or None when the fused kernel does not cover the finest propagator
+        (then the relaxation issues its two sweeps)."""
+        if not hasattr(self, "_fcf_ws"):
+            ws = None
+            nc = self.n_chunks0
+            if nc >= 2:
+                phi = self._phi(0, dev.regime_for_batch(nc))
+                nb = dev.fcf_workspace_bytes(phi, nc, self.options.m)
+                if nb > 0:
+                    ws = torch.zeros(nb, dtype=torch.uint8, device=self.device)
+            self._fcf_ws = ws
+        return self._fcf_ws
 
     def _reduce(self, n_chunks: int) -> tuple[float, float, float]:
         dev.sum_partials(self._partials, n_chunks, 3, self._sums)
@@ -259,15 +276,24 @@ class MgritHierarchy:
                           tail_out=dst[1], to_s=nx, what="c_relax")
             else:
                 src = self._fsrc
+                ws = self._fcf_workspace()
                 if self._cur == src:
                     d = self._other(src)
-                    self._c[d][0].copy_(self._c[src][0])
+                    if ws is None:
+                        self._c[d][0].copy_(self._c[src][0])
                     self._cur = d
                 dst = self._c[self._cur]
-                dev.sweep(phi, n_chunks=nc, start=self._c[src], start_stride=nx,
-                          n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
-                          tail_regime=regime, tail_g_mode=G_ZERO, tail_out=dst[1],
-                          to_s=nx, what="c_relax")
+                if ws is not None:
+                    # one launch, intervals split over persistent CTAs by step
+                    # (node 0 copied by the kernel)
+                    dev.relax_fcf(phi, n_chunks=nc, m=m, g_mode=G_ZERO, cs=self._c[src],
+                                  cd=dst, workspace=ws, segment=self._fcf_segment,
+                                  what="c_relax")
+                else:
+                    dev.sweep(phi, n_chunks=nc, start=self._c[src], start_stride=nx,
+                              n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
+                              tail_regime=regime, tail_g_mode=G_ZERO, tail_out=dst[1],
+                              to_s=nx, what="c_relax")
             self._pristine = False
             return
         n = self.n[l]
@@ -448,6 +474,35 @@ class MgritHierarchy:
                       what="fine_values")
         return out.view(nt + 1, self.n_components, self.n_cells)
 
+    def relax_fine_values(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """``relax(0)`` followed by ``fine_values(out)``: one FCF relaxation of
+        the finest level with the relaxed trajectory materialised.  With FCF
+        relaxation and a propagator the fused kernel covers, this is ONE
+        launch (mgp_relax_fcf): each interval's C-step runs straight into the
+        next interval's final F-steps and the work is split over persistent
+        CTAs; otherwise relax(0) and fine_values()."""
+        m, nx, nt = self.options.m, self.nx, self.n[0]
+        ws = self._fcf_workspace() if self.options.relaxation == "fcf" else None
+        if ws is None:
+            self.relax(0)
+            return self.fine_values(out=out)
+        if out is None:
+            out = torch.empty(nt + 1, nx, dtype=dev.DTYPE, device=self.device)
+        else:
+            out = out.view(nt + 1, nx)
+        self.f_relax(0)                   # F-points now derive from these C-points
+        src = self._cur
+        d = self._other(src)
+        nc = self.n_chunks0
+        dev.relax_fcf(self._phi(0, dev.regime_for_batch(nc)), n_chunks=nc, m=m, g_mode=G_ZERO,
+                      cs=self._c[src], cd=self._c[d], workspace=ws,
+                      segment=self._fcf_segment, fstore=out[1],
+                      f_cs=m * nx, f_ss=nx, cstore=out, cst_s=m * nx,
+                      what="relax_fine_values")
+        self._cur = self._fsrc = d
+        self._pristine = False
+        return out.view(nt + 1, self.n_components, self.n_cells)
+
     def load_c_points(self, c_points) -> None:
         """Set the finest-level C-points (N_t/m + 1 rows, host or device) and
         take the F-points as F-relaxed from them (the state after an
@@ -528,7 +583,17 @@ class MgritHierarchy:
                 cs[a:b + (1 if last else 0)].copy_(ch[a:b + (1 if last else 0)],
                                                    non_blocking=True)
             comp.wait_stream(h2d)
-            if fcf:
+            ws = self._fcf_workspace() if fcf else None
+            if ws is not None:
+                # one launch per piece: new C-points a+1..b into cd and the
+                # trajectory rows a*m .. b*m (interval a's final F-steps
+                # start from the new C-point a the previous piece wrote)
+                dev.relax_fcf(phi, n_chunks=b - a, m=m, g_mode=G_ZERO, cs=cs[a], cd=cd[a],
+                              workspace=ws, segment=self._fcf_segment,
+                              fstore=traj[a * m + 1], f_cs=m * nx, f_ss=nx,
+                              cstore=traj[a * m], cst_s=m * nx,
+                              f0_start=None if a == 0 else cd[a], what="relax_to_host")
+            elif fcf:
                 if a == 0:
                     cd[0].copy_(cs[0])
                 # fused F + C relaxation of chunks [a, b): new C-points a+1..b
@@ -536,11 +601,12 @@ class MgritHierarchy:
                           n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI, tail_regime=regime,
                           tail_g_mode=G_ZERO, tail_out=cd[a + 1], to_s=nx,
                           what="relax_to_host/fc")
-            # final F-relaxation with every node stored
-            traj[a * m: b * m + 1: m].copy_(cd[a:b + 1])
-            dev.sweep(phi, n_chunks=b - a, start=cd[a], start_stride=nx, n_steps=m - 1,
-                      g_mode=G_ZERO, store=traj[a * m + 1], st_cs=m * nx, st_ss=nx,
-                      what="relax_to_host/f")
+            if ws is None:
+                # final F-relaxation with every node stored
+                traj[a * m: b * m + 1: m].copy_(cd[a:b + 1])
+                dev.sweep(phi, n_chunks=b - a, start=cd[a], start_stride=nx, n_steps=m - 1,
+                          g_mode=G_ZERO, store=traj[a * m + 1], st_cs=m * nx, st_ss=nx,
+                          what="relax_to_host/f")
             d2h.wait_stream(comp)
             with torch.cuda.stream(d2h):
                 rows = slice(a * m, b * m + (1 if last else 0))

@@ -71,3 +71,23 @@ def test_abi_constants():
                       ("MGP_STATUS_NONPOSITIVE_DEPTH", _lib.STATUS_NONPOSITIVE_DEPTH),
                       ("MGP_SCHEME_RK_WENO_ROE", _lib.SCHEME_RK_WENO_ROE)]:
         assert re.search(rf"#define {name} {val}\b", hdr), name
+
+
+def test_fcf_args_layout_matches_c_compiler(tmp_path):
+    """The ctypes mirror of mgp_fcf_args against offsetof() from gcc on the
+    header itself."""
+    import subprocess
+    fields = [f[0] for f in _lib.MgpFcfArgs._fields_]
+    src = tmp_path / "layout.c"
+    body = "".join(f'    printf("%zu\\n", offsetof(mgp_fcf_args, {f}));\n' for f in fields)
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "mgrit_phi.h"\n'
+                   'int main(void) {\n    printf("%zu\\n", sizeof(mgp_fcf_args));\n'
+                   + body + "    return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(_lib.os.path.dirname(_lib.HEADER_PATH)), "-o", str(exe),
+                    str(src)], check=True)
+    vals = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True,
+                                           check=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(_lib.MgpFcfArgs)
+    for name, off in zip(fields, vals[1:]):
+        assert off == getattr(_lib.MgpFcfArgs, name).offset, name
