@@ -90,7 +90,7 @@ def test_relax_to_host_pieces_fused(segment):
     fused, plain = _pair(pb, segment)
     c_host = fused.c_points().reshape(-1, pb.n_x).cpu().pin_memory()
     out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
-    for pieces in (1, 2, 3, 1):             # workspace reused across interval counts
+    for pieces in (1, 2, 3, 1, 0):          # workspace reused; 0 = zero-copy launch
         fused.relax_to_host(c_host, out, pieces=pieces)
         torch.cuda.synchronize()
         plain.load_c_points(c_host)
