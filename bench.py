@@ -277,6 +277,7 @@ def run_ours(args):
 
     fused = not dist_path and h._fcf_workspace() is not None
     h._fcf_segment = int(os.environ.get("MGP_BENCH_SEGMENT", "0"))   # tuning experiments
+    h._fcf_split = int(os.environ.get("MGP_BENCH_SPLIT", "0"))       # 0 = automatic plan
 
     def step(record_kernels=False):
         if fused:

@@ -205,10 +205,13 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream);
  * i.e. exactly mgp_sweep(n_steps = m-1, TAIL_PHI) followed by
  * mgp_sweep(n_steps = m-1, store) on the new C-points, bit for bit.  Each
  * interval's C-step runs straight into the next interval's final F-steps
- * (one chain of 2m-1 steps), and single steps of the chains are handed to
- * persistent CTAs (one per resident slot) from a ticket counter; between
- * steps the field travels through an L2-resident ring in `workspace`, so
- * every slot stays busy to the end of the launch.  cd must not alias cs.
+ * (one chain of 2m-1 steps); persistent CTAs (one per resident slot) take
+ * whole chains from a ticket counter.  With more intervals than slots the
+ * first wave of chains runs only its F- and C-steps and queues the final
+ * F-steps (split plan), which later CTAs take in completion order, starting
+ * from the new C-point in cd; optionally the last chains are cut into
+ * segments handed over through an L2-resident ring (segment > 0).  cd must
+ * not alias cs.
  * workspace: at least mgp_relax_fcf_workspace() bytes, zero-filled once
  * before first use (every call leaves it clean again, so CUDA graph replays
  * work; calls sharing a workspace must be stream-ordered); epoch: non-zero
@@ -230,6 +233,12 @@ typedef struct mgp_fcf_args {
     uint32_t epoch;
     int32_t segment;      /* steps per hand-over segment of the chains taken
                              last (0 = whole chains, the measured default) */
+    int32_t split;        /* split plan with F-point storage and segment 0:
+                             0 = automatic (one CTA slot's worth of chains
+                             run F+C only and queue their final F-steps when
+                             intervals outnumber slots), -1 = off (whole
+                             chains), > 0 = that many split chains */
+    int32_t reserved;
 } mgp_fcf_args;
 int mgp_relax_fcf(const mgp_fcf_args *args, void *stream);
 /* Workspace bytes mgp_relax_fcf needs for this propagator and interval

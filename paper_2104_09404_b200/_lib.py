@@ -32,7 +32,7 @@ STATUS_NONPOSITIVE_DEPTH = 1
 STATUS_NONPOSITIVE_DENSITY = 2
 STATUS_NONPOSITIVE_PRESSURE = 4
 STATUS_ROE_NONHYPERBOLIC = 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -96,6 +96,7 @@ class MgpFcfArgs(ctypes.Structure):
         ("f0_start", _P),
         ("workspace", _P), ("workspace_bytes", _I64),
         ("epoch", ctypes.c_uint32), ("segment", _I32),
+        ("split", _I32), ("reserved", _I32),
     ]
 
 

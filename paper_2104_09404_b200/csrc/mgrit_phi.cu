@@ -1037,6 +1037,8 @@ struct FcfPlan {
     int64_t nc, nchains, W;   // intervals, chains (+1 with F-point storage), tickets
     int64_t K, R;             // chains taken whole; the last R = nchains - K are split
     int64_t Gmax;             // resident CTA slots (workspace layout)
+    int64_t A;                // split plan: chains 0..A-1 run their first m steps only
+                              // (F-steps + C-step) and queue their final F-steps
     int m, L, S;              // coarsening factor, regular chain length, segment steps
     bool fstore;
     __host__ __device__ int len(int64_t j) const {
@@ -1107,7 +1109,7 @@ template <int K, int REG, int MODEL, int P, int REGS>
 __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts k,
                                              const FcfPlan pl) {
     extern __shared__ double smem[];
-    __shared__ long long s_ticket;
+    __shared__ long long s_ticket, s_chain;
     using F = Field<K, REG, MODEL, P, 1>;
     F f;
     const int ns = (int)a.phi.nx;
@@ -1122,9 +1124,11 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
     f.s_u0 = f.s_R + sk_size(ns);
     f.s_red = reinterpret_cast<unsigned long long *>(f.s_u0 + sk_size(ns));
     // workspace (layout fixed per device and mesh, whatever the call's
-    // interval count): ticket and exit counters | Gmax tags | Gmax rows
+    // interval count): ticket, exit and queue counters, one spare | Gmax
+    // tags (segment mode) or queue slots (split plan) | Gmax rows
     unsigned long long *ctr = static_cast<unsigned long long *>(a.workspace);
-    unsigned long long *tags = ctr + 2;
+    unsigned long long *tags = ctr + 4;
+    unsigned long long *queue = tags;   // split plan (tags are segment-mode only)
     double *ring = reinterpret_cast<double *>(tags + pl.Gmax);
     const double *c0 = a.f0_start ? a.f0_start : a.cs;   // new C-point 0
     const int m = pl.m;
@@ -1146,13 +1150,38 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
 #endif
         int64_t j;
         int seg;
-        pl.unit(i, j, seg);
-        const int len = pl.len(j);
-        const int s0 = seg < 0 ? 0 : seg * pl.S;
-        const int s1 = (seg < 0 || s0 + pl.S >= len) ? len : s0 + pl.S;
+        int s0, s1, len;
+        const bool a_only = i < pl.A;              // split plan, first half
+        const bool b_unit = pl.A > 0 && i > pl.nc; // split plan, second half
+        if (b_unit) {
+            // the final F-steps of a chain whose first half has completed, in
+            // completion order (queue slot i - nc - 1; 0 = not yet published)
+            if (tid == 0) {
+                unsigned long long v;
+                while ((v = ld_acquire_u64(queue + (i - pl.nc - 1))) == 0ull) __nanosleep(64);
+                s_chain = (long long)v - 1;
+            }
+            __syncthreads();
+            j = s_chain;
+            seg = -1;
+            len = pl.L;
+            s0 = m;
+            s1 = pl.L;
+        } else {
+            if (a_only) {
+                j = i;
+                seg = -1;
+            } else {
+                pl.unit(i, j, seg);
+            }
+            len = pl.len(j);
+            s0 = seg < 0 ? 0 : seg * pl.S;
+            s1 = a_only ? m : (seg < 0 || s0 + pl.S >= len) ? len : s0 + pl.S;
+        }
+        const bool seg_mode = seg >= 0;
         const int64_t row = j - pl.K;               // split chains only
         double *rrow = ring + (row < 0 ? 0 : row) * ns;
-        if (s0 > 0) {
+        if (seg_mode && s0 > 0) {
             // a later segment needs the chain's previous one (taken about R
             // tickets earlier, normally long done)
             if (tid == 0)
@@ -1160,6 +1189,7 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
             __syncthreads();
         }
         if (s0 == 0) fcf_load(f, j == pl.nc ? c0 : a.cs + j * a.cs_s, ns, false);
+        else if (b_unit) fcf_load(f, a.cd + (j + 1) * a.cd_s, ns, true);
         else fcf_load(f, rrow, ns, true);
         for (int st = s0; st < s1; ++st) {
             f.sync();
@@ -1181,7 +1211,7 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
             } else if (st >= m) {                   // interval j+1's final F-steps
                 dst = a.fstore + (j + 1) * a.f_cs + (int64_t)(st - m) * a.f_ss;
             }
-            const bool hand = (st == s1 - 1) && (s1 < len);   // hand the field on
+            const bool hand = seg_mode && (st == s1 - 1) && (s1 < len);   // hand the field on
             for (int c = tid; c < ns; c += nt) {
                 const double v = add_g(f.result(c), a.g_mode, nullptr, c);
                 f.put(c, v);
@@ -1190,10 +1220,19 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
                 if (hand) __stcg(rrow + c, v);
             }
         }
-        if (s1 < len) {
+        if (seg_mode && s1 < len) {
             __threadfence();   // every thread's row stores before the release
             __syncthreads();
             if (tid == 0) st_release_u64(tags + row, fcf_tag(j, s1));
+        }
+        if (a_only) {
+            // new C-point j+1 is in cd: queue the chain's final F-steps
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                const unsigned long long pos = atomicAdd(ctr + 2, 1ull);
+                st_release_u64(queue + pos, (unsigned long long)j + 1);
+            }
         }
 #ifdef MGP_FCF_TRACE
         if (tid == 0 && i < 8192) {
@@ -1214,8 +1253,10 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
         const unsigned long long done = atomicAdd(ctr + 1, 1ull);
         if (done == (unsigned long long)gridDim.x - 1) {
             for (int64_t r = 0; r < pl.R; ++r) tags[r] = 0ull;
+            for (int64_t r = 0; r < pl.A; ++r) queue[r] = 0ull;
             ctr[0] = 0ull;
             ctr[1] = 0ull;
+            ctr[2] = 0ull;
             __threadfence();
         }
     }
@@ -2074,7 +2115,7 @@ int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
     if (G < 1) return MGP_EINVAL;
     L.G = (int)G;
     L.R = nchains > G ? G : 0;
-    L.bytes = (2 + L.Gmax) * 8 + L.Gmax * ns * (int64_t)sizeof(double);
+    L.bytes = (4 + L.Gmax) * 8 + L.Gmax * ns * (int64_t)sizeof(double);
     return MGP_OK;
 }
 
@@ -2098,6 +2139,20 @@ int fcf_launch(const mgp_fcf_args &a, cudaStream_t st) {
     // shapes: whole chains (S = L) and S = 1, 2 within 1-2 %
     pl.S = (a.segment > 0 && a.segment < pl.L) ? a.segment : pl.L;
     pl.W = pl.n_units();
+    // split plan (F-point storage, whole chains): with more intervals than
+    // CTA slots, the first A chains run only their F- and C-steps and queue
+    // their final F-steps, so the second wave draws from whole chains and
+    // 3-step units instead of idling on a partial wave of 7-step chains
+    pl.A = 0;
+    if (fstore && pl.S == pl.L && a.split >= 0 && pl.nc >= 2) {
+        int64_t A = a.split > 0 ? a.split : (pl.nc > L.G ? (int64_t)L.G : 0);
+        if (A > pl.nc - 1) A = pl.nc - 1;
+        if (A > L.Gmax) A = L.Gmax;          // queue slots
+        pl.A = A;
+        pl.K = pl.nchains;
+        pl.R = 0;
+        pl.W = pl.nchains + A;
+    }
     fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>
         <<<L.G, L.nt, L.smem, st>>>(a, make_consts(a.phi), pl);
     ++g_launches;
@@ -2279,7 +2334,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
 
 int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
-int32_t mgp_abi_version(void) { return 4; }
+int32_t mgp_abi_version(void) { return 5; }
 
 int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
     if (k < 0 || k > 3 || !cw16 || !d4 || !sm64) return MGP_EINVAL;

@@ -184,7 +184,7 @@ def fcf_workspace_bytes(phi: MgpPhi, n_chunks: int, m: int) -> int:
 def relax_fcf(phi: MgpPhi, *, n_chunks: int, m: int, g_mode: int, cs, cd, workspace,
               fstore=None, f_cs: int = 0, f_ss: int = 0, cstore=None, cst_s: int = 0,
               f0_start=None, cs_s: int | None = None, cd_s: int | None = None,
-              segment: int = 0, what: str = "mgp_relax_fcf"):
+              segment: int = 0, split: int = 0, what: str = "mgp_relax_fcf"):
     """One fused launch of the finest level's FCF relaxation (mgp_relax_fcf,
     include/mgrit_phi.h): new C-points into ``cd`` and, with ``fstore``, the
     relaxed iterate's F-points."""
@@ -200,5 +200,6 @@ def relax_fcf(phi: MgpPhi, *, n_chunks: int, m: int, g_mode: int, cs, cd, worksp
     a.workspace, a.workspace_bytes = ptr(workspace), int(workspace.numel())
     a.epoch = 1    # the kernel leaves its hand-over flags cleared
     a.segment = int(segment)
+    a.split = int(split)
     rc = _lib.load().mgp_relax_fcf(ctypes.byref(a), ctypes.c_void_p(stream_handle()))
     _lib.check(rc, what)

@@ -210,7 +210,9 @@ class MgritHierarchy:
         self._g = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
         self._phi_buf = torch.empty(max(n1, 1), nx, **kw)
         # fused FCF relaxation: steps per hand-over segment (0 = whole chains)
+        # and split plan (0 = automatic, -1 = whole chains only)
         self._fcf_segment = 0
+        self._fcf_split = 0
         self._partials = torch.empty(max(self.n[0] + 1, 1) * 3, **kw)
         self._sums = torch.empty(4, **kw)
 
@@ -287,7 +289,7 @@ class MgritHierarchy:
                     # one launch, intervals split over persistent CTAs by step
                     # (node 0 copied by the kernel)
                     dev.relax_fcf(phi, n_chunks=nc, m=m, g_mode=G_ZERO, cs=self._c[src],
-                                  cd=dst, workspace=ws, segment=self._fcf_segment,
+                                  cd=dst, workspace=ws, segment=self._fcf_segment, split=self._fcf_split,
                                   what="c_relax")
                 else:
                     dev.sweep(phi, n_chunks=nc, start=self._c[src], start_stride=nx,
@@ -496,7 +498,7 @@ class MgritHierarchy:
         nc = self.n_chunks0
         dev.relax_fcf(self._phi(0, dev.regime_for_batch(nc)), n_chunks=nc, m=m, g_mode=G_ZERO,
                       cs=self._c[src], cd=self._c[d], workspace=ws,
-                      segment=self._fcf_segment, fstore=out[1],
+                      segment=self._fcf_segment, split=self._fcf_split, fstore=out[1],
                       f_cs=m * nx, f_ss=nx, cstore=out, cst_s=m * nx,
                       what="relax_fine_values")
         self._cur = self._fsrc = d
@@ -554,7 +556,7 @@ class MgritHierarchy:
         th = traj_host.reshape(-1, nx)
         dev.relax_fcf(self._phi(0, dev.regime_for_batch(nc)), n_chunks=nc, m=m, g_mode=G_ZERO,
                       cs=c_points_host.reshape(-1, nx), cd=self._c[d], workspace=ws,
-                      segment=self._fcf_segment, fstore=th[1], f_cs=m * nx, f_ss=nx,
+                      segment=self._fcf_segment, split=self._fcf_split, fstore=th[1], f_cs=m * nx, f_ss=nx,
                       cstore=th, cst_s=m * nx, what="relax_to_host")
         self._cur = self._fsrc = d
         self._pristine = False
@@ -614,7 +616,7 @@ class MgritHierarchy:
                 # trajectory rows a*m .. b*m (interval a's final F-steps
                 # start from the new C-point a the previous piece wrote)
                 dev.relax_fcf(phi, n_chunks=b - a, m=m, g_mode=G_ZERO, cs=cs[a], cd=cd[a],
-                              workspace=ws, segment=self._fcf_segment,
+                              workspace=ws, segment=self._fcf_segment, split=self._fcf_split,
                               fstore=traj[a * m + 1], f_cs=m * nx, f_ss=nx,
                               cstore=traj[a * m], cst_s=m * nx,
                               f0_start=None if a == 0 else cd[a], what="relax_to_host")

@@ -14,7 +14,7 @@ from paper_2104_09404_b200 import device as dev
 pytestmark = pytest.mark.gpu
 
 
-def _pair(pb, segment=0):
+def _pair(pb, segment=0, split=0):
     u0 = pb.initial_state()
     tg = pb.time_grid(u0)
     steppers = pb.steppers(tg)
@@ -24,6 +24,7 @@ def _pair(pb, segment=0):
     plain = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
     plain._fcf_ws = None                     # force the two-sweep path
     fused._fcf_segment = segment
+    fused._fcf_split = split
     for h in (fused, plain):
         h.load_c_points(c)
     assert fused._fcf_workspace() is not None
@@ -55,6 +56,21 @@ def test_relax_fine_values_equals_two_sweeps(nx, nt, m, order, stepper, segment)
         plain.relax(0)
         want = plain.fine_values()
         assert torch.equal(got, want)
+        assert torch.equal(fused.c_points(), plain.c_points())
+
+
+@pytest.mark.parametrize("split", [-1, 0, 1, 7, 600, 100000])
+@pytest.mark.parametrize("nx,nt,m,order,stepper", [CASES[0], CASES[1], CASES[2], CASES[4]])
+def test_split_plan_equals_two_sweeps(nx, nt, m, order, stepper, split):
+    """Split plan: the first chains run F + C only and queue their final
+    F-steps, taken later in completion order from the new C-point in cd."""
+    pb = P.Problem(name="fcf-split", n_x=nx, n_t=nt, m=m, cfl=0.3, n_modes=4,
+                   weno_order=(order,), stepper=(stepper,))
+    fused, plain = _pair(pb, 0, split)
+    for _ in range(3):                       # both parities, workspace reused
+        got = fused.relax_fine_values()
+        plain.relax(0)
+        assert torch.equal(got, plain.fine_values())
         assert torch.equal(fused.c_points(), plain.c_points())
 
 
@@ -104,10 +120,10 @@ def test_workspace_query_and_rejections():
     tg = pb.time_grid(u0)
     phi = pb.steppers(tg)[0].phi_struct(dev.regime_for_batch(1024))
     nb = dev.fcf_workspace_bytes(phi, 1024, 4)
-    # two counters, then a tag word and a hand-over row per resident CTA slot
-    # (the layout does not depend on the interval count)
-    slots = (nb - 16) // (8 + 512 * 8)
-    assert nb == 16 + slots * (8 + 512 * 8) and 148 <= slots <= 148 * 16
+    # four counters, then a tag / queue word and a hand-over row per resident
+    # CTA slot (the layout does not depend on the interval count)
+    slots = (nb - 32) // (8 + 512 * 8)
+    assert nb == 32 + slots * (8 + 512 * 8) and 148 <= slots <= 148 * 16
     assert dev.fcf_workspace_bytes(phi, 8, 4) == nb
     lane2 = pb.steppers(tg)[0].phi_struct(dev.regime_for_batch(1))
     assert dev.fcf_workspace_bytes(lane2, 1024, 4) == 0     # single-field regime

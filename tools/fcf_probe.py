@@ -35,8 +35,13 @@ for nc in [int(x) for x in (sys.argv[1:] or "296 592 1024 1184 2368 4736".split(
     c = torch.from_numpy(u0).cuda().reshape(1, -1).expand(nc + 1, -1).contiguous()
     out = torch.empty(pb.n_t + 1, pb.n_x, dtype=torch.float64, device="cuda")
     row = {}
-    for name, fused in (("fused", True), ("two_sweeps", False)):
+    variants = [("fused_whole", True, -1), ("fused_split_auto", True, 0),
+                ("two_sweeps", False, 0)]
+    for sp in os.environ.get("MGP_PROBE_SPLITS", "").split():
+        variants.append((f"split_{sp}", True, int(sp)))
+    for name, fused, split in variants:
         h = P.MgritHierarchy(st, u0, tg, pb.space_grid(), pb.options())
+        h._fcf_split = split
         if not fused:
             h._fcf_ws = None
         h.load_c_points(c)

@@ -8,5 +8,5 @@ timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
 $CMD > gpurun_out/bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-ncu --set full --clock-control none -k regex:fcf_kernel -s 1 -c 1 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:fcf_kernel -s 1 -c 1 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full.log
