@@ -113,6 +113,10 @@ def build(verbose: bool = False) -> str:
            "-o", LIB_PATH, SRC_PATH]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    if os.environ.get("MGP_FAST_BUILD") == "1":
+        # development builds: nvcc splits the optimiser over all host cores
+        # (~4x faster; the SASS schedule differs slightly from the release build)
+        cmd.insert(1, "-split-compile=0")
     subprocess.run(cmd, check=True)
     return LIB_PATH
 

@@ -1017,6 +1017,242 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
 }
 
 // ---------------------------------------------------------------------------
+// Sequential march of ONE field over a thread-block cluster (coarse solve
+// mgrit.py:219-226, serial solve serial.py:40-61) with ONE cluster barrier
+// per Runge-Kutta stage.  CTA q owns the slab of cells [c0, c0 + ns) and
+// also keeps G = K+1 ghost cells on each side, which it updates itself: the
+// interface states its neighbours computed next to its slab (G+1 on the
+// left, G on the right) arrive through distributed shared memory together
+// with alpha, before the one barrier, so the ghost cells' fluxes, rhs and
+// Runge-Kutta updates are formed locally with the neighbours' exact
+// operations (bit-identical values) and the next stage needs no halo
+// exchange.  Per stage: reconstruction of the owned interfaces (two
+// threads per interface, one per side, as the latency mode of Field), warp
+// max -> the alpha slots of every CTA, the barrier, alpha from the slots,
+// then one thread per held cell forms both of its interface fluxes and the
+// stage value.  Interface states and alpha slots are double-buffered by
+// stage parity (a CTA is at most one barrier ahead of its neighbours).
+// Same arithmetic as Field::phi + sweep_body (bit-identical); used for
+// plain marches (no tail, no partial sums, no repeats).
+// ---------------------------------------------------------------------------
+#ifndef MGP_MARCH_SPLIT
+#define MGP_MARCH_SPLIT 0   // 1: split cluster barrier with the rhs-free RK terms in between
+#endif
+template <int K, int REG, int CS>
+__global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, const Consts k) {
+    constexpr int G = K + 1;   // ghost cells per side
+    constexpr int IL = G + 1;  // interfaces held left of the slab: local [-IL, -1]
+    constexpr int IR = G;      // and right of it: [ns, ns + IR)
+    extern __shared__ double smem[];
+    const int nx = (int)a.phi.nx;
+    const int ns = nx / CS;
+    const int q = (int)(blockIdx.x % CS);
+    const int c0 = q * ns;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int ncell = ns + 2 * G;         // cells held: local [-G, ns + G)
+    const int ni = ns + IL + IR;          // interfaces held: local [-IL, ns + IR)
+    double *s_u0 = smem;                  // RK base, local cell t at [t + G]
+    double *s_v = s_u0 + ncell;           // stage input
+    double *s_L = s_v + ncell;            // [2][ni] left states, interface i at [i + IL]
+    double *s_R = s_L + 2 * ni;           // [2][ni] right states
+    // [2][CS][warps] alpha bits by stage parity: every warp of the cluster
+    // stores its max into its slot of every CTA
+    unsigned long long *s_am = reinterpret_cast<unsigned long long *>(s_R + 2 * ni);
+    cg::cluster_group cl = cg::this_cluster();
+    double *rl_L = cl.map_shared_rank(s_L, (q + CS - 1) % CS);
+    double *rl_R = cl.map_shared_rank(s_R, (q + CS - 1) % CS);
+    double *rr_L = cl.map_shared_rank(s_L, (q + 1) % CS);
+    double *rr_R = cl.map_shared_rank(s_R, (q + 1) % CS);
+    unsigned long long *r_am = cl.map_shared_rank(s_am, lane < CS ? lane : 0);
+
+    for (int t = tid - G; t < ns + G; t += nt) {
+        int c = c0 + t;
+        c = c < 0 ? c + nx : (c >= nx ? c - nx : c);
+        const double v = a.start[c];
+        s_u0[t + G] = v;
+        s_v[t + G] = v;
+    }
+    cl.sync();   // every CTA of the cluster running and loaded
+
+    const int side = warp & 1;                     // warp-uniform
+    const int i = ((warp >> 1) << 5) + lane;       // interface i + 1/2 (local)
+    const int t = tid - G;                         // held cell of the update phase
+    int cg_ = c0 + t;                              // its global index (periodic)
+    cg_ = cg_ < 0 ? cg_ + nx : (cg_ >= nx ? cg_ - nx : cg_);
+    const bool upd = t < ns + G;
+    const bool own = t >= 0 && t < ns;
+    const int rk = a.phi.rk_order;
+    const int stages = rk == 0 ? 1 : rk;
+    int par = 0;
+#ifdef MGP_TRACE
+    long long prof[6] = {0, 0, 0, 0, 0, 0}, pt0 = clock64(), pt1;
+#define MARCH_PROF(ph) do { pt1 = clock64(); prof[ph] += pt1 - pt0; pt0 = pt1; } while (0)
+#else
+#define MARCH_PROF(ph) do { } while (0)
+#endif
+    for (int s = 1; s <= a.n_steps; ++s) {
+        // this step's g, loaded ahead of the stages that hide its latency
+        double gv = 0.0;
+        if (upd && a.g_mode == MGP_G_ARRAY) gv = a.g[(int64_t)(s - 1) * a.g_ss + cg_];
+        for (int sg = 0; sg < stages; ++sg, par ^= 1) {
+            double *L = s_L + par * ni, *R = s_R + par * ni;
+            unsigned long long m = 0;
+            if (i < ns) {
+                const int ctr = i + side;          // window centre
+                double win[2 * K + 1];
+#pragma unroll
+                for (int w = 0; w <= 2 * K; ++w) win[w] = s_v[ctr - K + w + G];
+                bool badw = false;
+#pragma unroll
+                for (int w = 0; w <= 2 * K; ++w) badw |= !is_finite(win[w]);
+                double b[K + 1], qv[K + 1];
+                if (side == 0) {
+#pragma unroll
+                    for (int s2 = 0; s2 <= K; ++s2) {
+                        double dummy;
+                        beta_block<K, false, true>(win, s2, b[s2], dummy);
+                    }
+#pragma unroll
+                    for (int r = 0; r <= K; ++r) qv[r] = cand_left<K, REG>(win, r);
+                } else {
+#pragma unroll
+                    for (int s2 = 0; s2 <= K; ++s2) {
+                        double dummy;
+                        beta_block<K, true, false>(win, s2, dummy, b[K - s2]);
+                    }
+#pragma unroll
+                    for (int r = 0; r <= K; ++r) qv[r] = cand_right<K, REG>(win, r);
+                }
+                const double v = weno_value<K>(b, qv, k.eps, nullptr, badw);
+                const int o = par * ni;
+                (side == 0 ? L : R)[i + IL] = v;
+                if (i < IR) (side == 0 ? rl_L : rl_R)[o + ns + i + IL] = v;
+                if (i >= ns - IL) (side == 0 ? rr_L : rr_R)[o + i - ns + IL] = v;
+                m = abs_bits(v);
+                // a non-finite cell makes the reference's alpha NaN
+                if (side == 0 && !is_finite(win[K])) m = kNaNBits;
+            }
+            MARCH_PROF(0);
+            m = warp_umax64(m);
+            if (lane < CS) r_am[par * CS * nw + q * nw + warp] = m;
+            MARCH_PROF(1);
+#if MGP_MARCH_SPLIT
+            // release: states, ghosts' interfaces, alpha; the work between
+            // arrive and wait touches only this thread's own cells
+            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#else
+            cl.sync();   // release / acquire: states, ghosts' interfaces, alpha slots
+#endif
+#if MGP_MARCH_SPLIT
+            double u0 = 0.0, stg = 0.0, base = 0.0;
+            if (upd) {
+                u0 = s_u0[tid];
+                stg = s_v[tid];
+                // the Runge-Kutta terms that do not involve the rhs
+                if (rk == 0 || sg == 0) base = u0;
+                else if (rk == 2) base = (0.5 * u0) + (0.5 * stg);
+                else if (sg == 1) base = (0.75 * u0) + (0.25 * stg);
+                else base = (u0 / 3.0) + (k.two3 * stg);
+            }
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
+            MARCH_PROF(2);
+            unsigned long long mm = 0;
+            for (int l = lane; l < CS * nw; l += 32) mm = umax64(mm, s_am[par * CS * nw + l]);
+            mm = warp_umax64(mm);
+            const double half_alpha = 0.5 * __longlong_as_double((long long)mm);
+            MARCH_PROF(3);
+            if (upd) {
+                // flux.py:82-88 (Burgers f = (0.5 u) u), flux.py:159-161
+                const double ulp = L[t + IL], urp = R[t + IL];
+                const double ulm = L[t - 1 + IL], urm = R[t - 1 + IL];
+                const double fp = (0.5 * ((0.5 * ulp) * ulp + (0.5 * urp) * urp)) -
+                                  (half_alpha * (urp - ulp));
+                const double fm = (0.5 * ((0.5 * ulm) * ulm + (0.5 * urm) * urm)) -
+                                  (half_alpha * (urm - ulm));
+                const double neg = -(fp - fm);
+                const double A = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+                double st;
+#if MGP_MARCH_SPLIT
+                if (rk == 0) st = A;
+                else if (sg == 0) st = base + k.dt * A;
+                else if (rk == 2) st = base + (k.hdt * A);
+                else if (sg == 1) st = base + (k.qdt * A);
+                else st = base + (k.tdt * A);
+#else
+                const double u0 = s_u0[tid], stg = s_v[tid];
+                if (rk == 0) st = A;
+                else if (sg == 0) st = u0 + k.dt * A;
+                else if (rk == 2) st = ((0.5 * u0) + (0.5 * stg)) + (k.hdt * A);
+                else if (sg == 1) st = ((0.75 * u0) + (0.25 * stg)) + (k.qdt * A);
+                else st = ((u0 / 3.0) + (k.two3 * stg)) + (k.tdt * A);
+#endif
+                if (sg == stages - 1) {
+                    // sweep_body: + g, store, next step's base
+                    if (a.g_mode == MGP_G_ZERO) st = st + 0.0;
+                    else if (a.g_mode == MGP_G_ARRAY) st = st + gv;
+                    if (own && a.store) a.store[(int64_t)(s - 1) * a.st_ss + c0 + t] = st;
+                    s_u0[tid] = st;
+                }
+                s_v[tid] = st;
+            }
+            MARCH_PROF(4);
+            __syncthreads();
+            MARCH_PROF(5);
+        }
+    }
+#ifdef MGP_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int ph = 0; ph < 6; ++ph) {
+            g_trace[2 * ph] = ph;
+            g_trace[2 * ph + 1] = prof[ph];
+        }
+        g_trace_n = 6;
+    }
+#endif
+#undef MARCH_PROF
+}
+
+Consts make_consts(const mgp_phi &p);
+
+template <int K, int REG, int CS>
+int launch_march(const mgp_sweep_args &a, cudaStream_t st) {
+    const int ns = (int)(a.phi.nx / CS);
+    const int nt = 2 * ((ns + 31) / 32 * 32);
+    const int G = K + 1;
+    const size_t sm = sizeof(double) * (size_t)(2 * (ns + 2 * G) + 4 * (ns + 2 * G + 1)) +
+                      sizeof(unsigned long long) * (size_t)(2 * CS * (nt / 32));
+    auto kern = march_kernel<K, REG, CS>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024) != cudaSuccess)
+            return MGP_ECUDA;
+        if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                           1) != cudaSuccess)
+            return MGP_ECUDA;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)CS);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const Consts kk = make_consts(a.phi);
+    if (cudaLaunchKernelEx(&cfg, kern, a, kk) != cudaSuccess) return MGP_ECUDA;
+    ++g_launches;
+    return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
 // Fused FCF relaxation of the finest level (mgp_relax_fcf, include/
 // mgrit_phi.h).  Chain j (j < nc) = interval j's m-1 F-steps, its C-step
 // (new C-point j+1) and, with F-point storage, interval j+1's m-1 final
@@ -1937,6 +2173,37 @@ int cluster_size(const mgp_sweep_args &a) {
     return 1;
 }
 
+// Cluster size of the one-barrier-per-stage march (march_kernel), or 0 when
+// the call is not a plain single-field march it covers.  Slabs of >= 64
+// cells (MGP_MARCH_MIN_SLAB; measured on B200: nx = 512 -> 8 CTAs 3.6 us per
+// WENO5/RK3 step, 16 CTAs 3.75; nx = 4096 -> 16 CTAs 6.6), at most 16 CTAs
+// and 256 cells per CTA;
+// MGP_MARCH_CS forces the size, MGP_MARCH2=0 selects the Field path.
+int march_cluster_size(const mgp_sweep_args &a) {
+    static int on = -1, min_slab = -1, force = -1;
+    if (on < 0) {
+        const char *e = getenv("MGP_MARCH2");
+        on = (e && atoi(e) == 0) ? 0 : 1;
+        min_slab = env_int("MGP_MARCH_MIN_SLAB");
+        if (min_slab <= 0) min_slab = 64;
+        force = env_int("MGP_MARCH_CS");
+    }
+    const int64_t nx = a.phi.nx;
+    if (!on || a.n_chunks != 1 || a.tail != MGP_TAIL_NONE || a.phi.repeats != 1 || a.ref ||
+        a.count_nonfinite || a.partials || a.n_steps < 1 || a.phi.weno_k != 2 ||
+        a.phi.model != MGP_MODEL_BURGERS || a.phi.scheme != MGP_SCHEME_RK_WENO ||
+        a.phi.rk_order < 0 || a.phi.rk_order > 3 ||
+        (a.g_mode != MGP_G_NONE && a.g_mode != MGP_G_ZERO && a.g_mode != MGP_G_ARRAY) ||
+        (a.g_mode == MGP_G_ARRAY && !a.g))
+        return 0;
+    int cs = force > 0 ? force : 16;
+    if (force <= 0)
+        while (cs > 2 && (nx % cs || nx / cs < min_slab)) cs /= 2;
+    if (cs != 2 && cs != 4 && cs != 8 && cs != 16) return 0;
+    if (nx % cs || nx / cs < 8 || nx / cs > 256) return 0;
+    return cs;
+}
+
 template <int K, int REG, int MODEL, int P>
 int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
 #ifdef MGP_EXPERIMENT
@@ -1969,6 +2236,15 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
         return MGP_EINVAL;
     }
 #else
+    if constexpr (K == 2 && MODEL == MGP_MODEL_BURGERS) {
+        switch (march_cluster_size(a)) {
+            case 2: return launch_march<K, REG, 2>(a, st);
+            case 4: return launch_march<K, REG, 4>(a, st);
+            case 8: return launch_march<K, REG, 8>(a, st);
+            case 16: return launch_march<K, REG, 16>(a, st);
+            default: break;
+        }
+    }
     if (cs > 1) {
       if constexpr (K != 2 || MODEL != MGP_MODEL_BURGERS) {
         return MGP_EINVAL;

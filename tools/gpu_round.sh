@@ -10,3 +10,5 @@ $CMD > gpurun_out/bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:fcf_kernel -s 1 -c 1 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+timeout 600 python tools/iter_times.py c2 c3 c5 > gpurun_out/iter_times.json 2> gpurun_out/iter_times.err; echo "iter rc=$?" >> gpurun_out/iter_times.err
+timeout 300 python tools/kernel_times.py c2 c3 > gpurun_out/kernel_times.json 2>&1
