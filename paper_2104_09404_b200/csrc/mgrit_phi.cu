@@ -1035,9 +1035,6 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
 // Same arithmetic as Field::phi + sweep_body (bit-identical); used for
 // plain marches (no tail, no partial sums, no repeats).
 // ---------------------------------------------------------------------------
-#ifndef MGP_MARCH_SPLIT
-#define MGP_MARCH_SPLIT 0   // 1: split cluster barrier with the rhs-free RK terms in between
-#endif
 template <int K, int REG, int CS>
 __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, const Consts k) {
     constexpr int G = K + 1;   // ghost cells per side
@@ -1137,26 +1134,7 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
             m = warp_umax64(m);
             if (lane < CS) r_am[par * CS * nw + q * nw + warp] = m;
             MARCH_PROF(1);
-#if MGP_MARCH_SPLIT
-            // release: states, ghosts' interfaces, alpha; the work between
-            // arrive and wait touches only this thread's own cells
-            asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-#else
             cl.sync();   // release / acquire: states, ghosts' interfaces, alpha slots
-#endif
-#if MGP_MARCH_SPLIT
-            double u0 = 0.0, stg = 0.0, base = 0.0;
-            if (upd) {
-                u0 = s_u0[tid];
-                stg = s_v[tid];
-                // the Runge-Kutta terms that do not involve the rhs
-                if (rk == 0 || sg == 0) base = u0;
-                else if (rk == 2) base = (0.5 * u0) + (0.5 * stg);
-                else if (sg == 1) base = (0.75 * u0) + (0.25 * stg);
-                else base = (u0 / 3.0) + (k.two3 * stg);
-            }
-            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-#endif
             MARCH_PROF(2);
             unsigned long long mm = 0;
             for (int l = lane; l < CS * nw; l += 32) mm = umax64(mm, s_am[par * CS * nw + l]);
@@ -1174,20 +1152,12 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
                 const double neg = -(fp - fm);
                 const double A = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
                 double st;
-#if MGP_MARCH_SPLIT
-                if (rk == 0) st = A;
-                else if (sg == 0) st = base + k.dt * A;
-                else if (rk == 2) st = base + (k.hdt * A);
-                else if (sg == 1) st = base + (k.qdt * A);
-                else st = base + (k.tdt * A);
-#else
                 const double u0 = s_u0[tid], stg = s_v[tid];
                 if (rk == 0) st = A;
                 else if (sg == 0) st = u0 + k.dt * A;
                 else if (rk == 2) st = ((0.5 * u0) + (0.5 * stg)) + (k.hdt * A);
                 else if (sg == 1) st = ((0.75 * u0) + (0.25 * stg)) + (k.qdt * A);
                 else st = ((u0 / 3.0) + (k.two3 * stg)) + (k.tdt * A);
-#endif
                 if (sg == stages - 1) {
                     // sweep_body: + g, store, next step's base
                     if (a.g_mode == MGP_G_ZERO) st = st + 0.0;
@@ -2159,8 +2129,7 @@ int cluster_size(const mgp_sweep_args &a) {
         return cs;
     }
     if (cl_ok && a.n_chunks == 1) {
-        static int env = -1;
-        if (env < 0) env = env_int("MGP_MARCH_CS");
+        const int env = env_int("MGP_MARCH_CS");   // per call (tests switch it)
         // default: slabs of >= 64 cells, at most 16 CTAs (measured, latency
         // mode: C2 nx=512 -> 8 CTAs, 5.5 us/step; C3 nx=4096 -> 16 CTAs,
         // 9.0 us/step)
@@ -2180,14 +2149,12 @@ int cluster_size(const mgp_sweep_args &a) {
 // and 256 cells per CTA;
 // MGP_MARCH_CS forces the size, MGP_MARCH2=0 selects the Field path.
 int march_cluster_size(const mgp_sweep_args &a) {
-    static int on = -1, min_slab = -1, force = -1;
-    if (on < 0) {
-        const char *e = getenv("MGP_MARCH2");
-        on = (e && atoi(e) == 0) ? 0 : 1;
-        min_slab = env_int("MGP_MARCH_MIN_SLAB");
-        if (min_slab <= 0) min_slab = 64;
-        force = env_int("MGP_MARCH_CS");
-    }
+    // read per call (a getenv per launch), so tests can switch paths in-process
+    const char *e = getenv("MGP_MARCH2");
+    const int on = (e && atoi(e) == 0) ? 0 : 1;
+    int min_slab = env_int("MGP_MARCH_MIN_SLAB");
+    if (min_slab <= 0) min_slab = 64;
+    const int force = env_int("MGP_MARCH_CS");
     const int64_t nx = a.phi.nx;
     if (!on || a.n_chunks != 1 || a.tail != MGP_TAIL_NONE || a.phi.repeats != 1 || a.ref ||
         a.count_nonfinite || a.partials || a.n_steps < 1 || a.phi.weno_k != 2 ||
