@@ -1103,6 +1103,11 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
                 bool badw = false;
 #pragma unroll
                 for (int w = 0; w <= 2 * K; ++w) badw |= !is_finite(win[w]);
+                double v;
+                if constexpr (K == 0) {
+                    // first order: beta = 0, omega = raw/raw (Field::reconstruct)
+                    v = k.k0_omega * (CW(0, 0, 0) * win[0]);
+                } else {
                 double b[K + 1], qv[K + 1];
                 if (side == 0) {
 #pragma unroll
@@ -1121,7 +1126,8 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
 #pragma unroll
                     for (int r = 0; r <= K; ++r) qv[r] = cand_right<K, REG>(win, r);
                 }
-                const double v = weno_value<K>(b, qv, k.eps, nullptr, badw);
+                v = weno_value<K>(b, qv, k.eps, nullptr, badw);
+                }
                 const int o = par * ni;
                 (side == 0 ? L : R)[i + IL] = v;
                 if (i < IR) (side == 0 ? rl_L : rl_R)[o + ns + i + IL] = v;
@@ -2143,21 +2149,25 @@ int cluster_size(const mgp_sweep_args &a) {
 }
 
 // Cluster size of the one-barrier-per-stage march (march_kernel), or 0 when
-// the call is not a plain single-field march it covers.  Slabs of >= 64
-// cells (MGP_MARCH_MIN_SLAB; measured on B200: nx = 512 -> 8 CTAs 3.6 us per
-// WENO5/RK3 step, 16 CTAs 3.75; nx = 4096 -> 16 CTAs 6.6), at most 16 CTAs
-// and 256 cells per CTA;
+// the call is not a plain single-field march it covers (Burgers RK-WENO,
+// WENO1/3/5).  Slabs of >= 64 cells (first order: 128; MGP_MARCH_MIN_SLAB),
+// at most 16 CTAs and 256 cells per CTA.  Measured on B200, us per SSP-RK3
+// step (profiles/r01_march2.txt), Field path -> march_kernel:
+//   WENO5 nx 512  4.99 -> 3.32 (8 CTAs)   nx 1024 5.89 -> 3.73 (16)  nx 4096 9.0 -> 6.29 (16)
+//   WENO3 nx 512  4.25 -> 3.05 (8)        nx 1024 6.91 -> 3.36 (16)  nx 4096 20.1 -> 5.24 (16)
+//   WENO1 nx 512  3.22 -> 2.31 (4)        nx 1024 4.01 -> 2.76 (8)   nx 4096 11.2 -> 4.63 (16)
 // MGP_MARCH_CS forces the size, MGP_MARCH2=0 selects the Field path.
 int march_cluster_size(const mgp_sweep_args &a) {
     // read per call (a getenv per launch), so tests can switch paths in-process
     const char *e = getenv("MGP_MARCH2");
     const int on = (e && atoi(e) == 0) ? 0 : 1;
     int min_slab = env_int("MGP_MARCH_MIN_SLAB");
-    if (min_slab <= 0) min_slab = 64;
+    if (min_slab <= 0) min_slab = a.phi.weno_k == 0 ? 128 : 64;
     const int force = env_int("MGP_MARCH_CS");
     const int64_t nx = a.phi.nx;
     if (!on || a.n_chunks != 1 || a.tail != MGP_TAIL_NONE || a.phi.repeats != 1 || a.ref ||
-        a.count_nonfinite || a.partials || a.n_steps < 1 || a.phi.weno_k != 2 ||
+        a.count_nonfinite || a.partials || a.n_steps < 1 ||
+        a.phi.weno_k < 0 || a.phi.weno_k > 2 ||
         a.phi.model != MGP_MODEL_BURGERS || a.phi.scheme != MGP_SCHEME_RK_WENO ||
         a.phi.rk_order < 0 || a.phi.rk_order > 3 ||
         (a.g_mode != MGP_G_NONE && a.g_mode != MGP_G_ZERO && a.g_mode != MGP_G_ARRAY) ||
@@ -2203,7 +2213,7 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
         return MGP_EINVAL;
     }
 #else
-    if constexpr (K == 2 && MODEL == MGP_MODEL_BURGERS) {
+    if constexpr (K <= 2 && MODEL == MGP_MODEL_BURGERS) {
         switch (march_cluster_size(a)) {
             case 2: return launch_march<K, REG, 2>(a, st);
             case 4: return launch_march<K, REG, 4>(a, st);

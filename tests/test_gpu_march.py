@@ -2,7 +2,8 @@
 of one field over a thread-block cluster (coarse solve mgrit.py:219-226,
 serial solve serial.py:40-61) -- against the two-barrier Field path and the
 CPU oracle's march, bit for bit (NaN-aware), for every cluster size it
-accepts, both summation regimes, every Runge-Kutta order and every g mode.
+accepts, first order, WENO3 and WENO5, both summation regimes, every Runge-Kutta order
+and every g mode.
 The path is selected per call through MGP_MARCH2 / MGP_MARCH_CS (read by
 the library at each launch)."""
 import os
@@ -19,9 +20,9 @@ from paper_2104_09404_b200._lib import G_ARRAY, G_NONE, G_ZERO, SUM_LANE2, SUM_S
 pytestmark = pytest.mark.gpu
 
 
-def _phi(nx, rk, regime, cfl=0.3):
+def _phi(nx, rk, regime, cfl=0.3, order=5):
     op = P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, nx),
-                                P.FluxConfig("lf", P.WenoConfig(5)))
+                                P.FluxConfig("lf", P.WenoConfig(order)))
     st = P.RungeKuttaStepper(op.rhs, cfl / nx, rk)
     return st.phi_struct(regime), cfl / nx
 
@@ -77,8 +78,9 @@ CASES = [(nx, cs) for nx in (32, 64, 128, 512, 1024, 4096) for cs in (2, 4, 8, 1
 @pytest.mark.parametrize("nx,cs", CASES)
 @pytest.mark.parametrize("rk", [1, 2, 3])
 @pytest.mark.parametrize("regime", [SUM_LANE2, SUM_SEQ])
-def test_march_kernel_equals_field_path(nx, cs, rk, regime):
-    phi, _ = _phi(nx, rk, regime)
+@pytest.mark.parametrize("order", [1, 3, 5])
+def test_march_kernel_equals_field_path(nx, cs, rk, regime, order):
+    phi, _ = _phi(nx, rk, regime, order=order)
     u0 = _field(nx, nx + cs + rk)
     n = 24
     got = _run(phi, u0, n, G_NONE, None, {"MGP_MARCH_CS": str(cs)})
@@ -88,9 +90,11 @@ def test_march_kernel_equals_field_path(nx, cs, rk, regime):
 
 @pytest.mark.parametrize("g_mode", [G_NONE, G_ZERO, G_ARRAY])
 @pytest.mark.parametrize("bad", [None, "nan", "inf", "huge"])
-def test_march_kernel_equals_oracle(g_mode, bad):
+@pytest.mark.parametrize("order", [1, 3, 5])
+def test_march_kernel_equals_oracle(g_mode, bad, order):
     nx, n, rk = 128, 16, 3
-    phi, dt = _phi(nx, rk, SUM_LANE2)
+    k = order // 2
+    phi, dt = _phi(nx, rk, SUM_LANE2, order=order)
     u0 = _field(nx, 7, bad)
     g = None
     if g_mode == G_ARRAY:
@@ -100,7 +104,7 @@ def test_march_kernel_equals_oracle(g_mode, bad):
         got = _run(phi, u0, n, g_mode, gd, {"MGP_MARCH_CS": str(cs)})
         want = np.empty((n + 1, nx))
         want[0] = u0
-        p = oracle.make_params(k=2, rk_order=rk, dt=dt, dx=1.0 / nx, regime=SUM_LANE2)
+        p = oracle.make_params(k=k, rk_order=rk, dt=dt, dx=1.0 / nx, regime=SUM_LANE2)
         gz = None
         if g_mode == G_ARRAY:
             gz = g.copy()
