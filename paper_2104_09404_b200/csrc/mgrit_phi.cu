@@ -438,6 +438,7 @@ struct Field {
     unsigned long long *s_cmax;    // [CS] per-CTA alpha bits
     double *r_u_left, *r_u_right;  // neighbours' s_u (distributed shared memory)
     double *r_edge_right;          // right neighbour's s_edge
+    double *r_L_right;             // right neighbour's s_L (centred reconstruction)
     // barrier over the CTAs sharing the field (hardware cluster barrier; an
     // mbarrier-based all-to-all with one arriving thread per CTA measured
     // 1.8-2.5x slower per stage on B200)
@@ -446,14 +447,18 @@ struct Field {
     static constexpr int HALO = H;
     __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
     __device__ __forceinline__ void load(int t, double v) { s_u[sk(t + H)] = v; }
-    // centred reconstruction with the merged flux / rhs pass (CS = 1): the
-    // interface states stay readable by neighbouring runs until the stage
-    // ends, so results go to the RK base slots, which only their owner reads
+    // centred reconstruction with the merged flux / rhs pass: the interface
+    // states stay readable by neighbouring runs until the stage ends, so
+    // results go to the RK base slots, which only their owner reads.  On a
+    // cluster (CS > 1) the slab's last window (centred on the right
+    // neighbour's cell 0) is the neighbour's left state of its interface 0,
+    // pushed into its s_L; the states of the interface left of the slab
+    // arrive in s_edge as before.
     static constexpr bool kMerged =
 #ifdef MGP_SLIDING_RECON
         false;
 #else
-        CS == 1 && P > 0 && K > 0;
+        P > 0 && K > 0;
 #endif
     __device__ __forceinline__ double result(int t) const {
         return kMerged ? s_u0[sk(t)] : s_R[sk(t)];
@@ -655,7 +660,15 @@ struct Field {
                 ul = __longlong_as_double(kNaNBits);
                 ur = ul;
             }
-            s_L[sk(c == ns ? 0 : c)] = ul;
+            if (CS == 1) {
+                s_L[sk(c == ns ? 0 : c)] = ul;
+            } else if (c == ns) {
+                r_L_right[sk(0)] = ul;      // L state of the neighbour's interface 0
+                r_edge_right[1] = ur;       // R state of the slab's last interface
+            } else {
+                s_L[sk(c)] = ul;
+                if (c == ns - 1) r_edge_right[0] = ul;
+            }
             s_R[sk(c - 1)] = ur;
             if (burg) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
@@ -738,7 +751,9 @@ struct Field {
             // barrier and a re-read
             if (i0 < ns) {
                 const int il = (i0 == 0) ? ns - 1 : i0 - 1;
-                double fm = lf(k, s_L[sk(il)], s_R[sk(il)], half_alpha);
+                double fm = (CS > 1 && i0 == 0)
+                                ? lf(k, s_edge[0], s_edge[1], half_alpha)
+                                : lf(k, s_L[sk(il)], s_R[sk(il)], half_alpha);
 #pragma unroll
                 for (int p = 0; p < PC; ++p) {
                     const int c = i0 + p;
@@ -1012,6 +1027,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
         f.r_u_left = cl.map_shared_rank(f.s_u, (q + CS - 1) % CS);
         f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
         f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
+        f.r_L_right = cl.map_shared_rank(f.s_L, (q + 1) % CS);
     }
     sweep_body<F, CS>(a, k, f, ns, q, c0, s_sum, s_psum, nx);
 }

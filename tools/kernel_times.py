@@ -35,6 +35,8 @@ for name in sys.argv[1:] or ["c2", "c3"]:
     st = pb.steppers(tg)[0]
     nx, m = pb.n_x, pb.m
     nc = pb.n_t // m
+    if os.environ.get("MGP_KT_MAXCHUNKS"):   # C5: a bounded sample of the intervals
+        nc = min(nc, int(os.environ["MGP_KT_MAXCHUNKS"]))
     x = dev.to_device(u0).reshape(nx).expand(nc, nx).contiguous()
     y = torch.empty_like(x)
     phi = st.phi_struct(0)
