@@ -1116,9 +1116,6 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
                 double win[2 * K + 1];
 #pragma unroll
                 for (int w = 0; w <= 2 * K; ++w) win[w] = s_v[ctr - K + w + G];
-                bool badw = false;
-#pragma unroll
-                for (int w = 0; w <= 2 * K; ++w) badw |= !is_finite(win[w]);
                 double v;
                 if constexpr (K == 0) {
                     // first order: beta = 0, omega = raw/raw (Field::reconstruct)
@@ -1142,7 +1139,9 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
 #pragma unroll
                     for (int r = 0; r <= K; ++r) qv[r] = cand_right<K, REG>(win, r);
                 }
-                v = weno_value<K>(b, qv, k.eps, nullptr, badw);
+                // one range test validates every fast-path division; a
+                // window with a non-finite cell is moot (alpha NaN)
+                v = weno_value_rc<K>(b, qv, k.eps, win);
                 }
                 const int o = par * ni;
                 (side == 0 ? L : R)[i + IL] = v;
