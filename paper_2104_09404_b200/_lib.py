@@ -106,18 +106,39 @@ EXPORTED_SYMBOLS = ("mgp_sweep", "mgp_sum_partials", "mgp_max_nx",
                     "mgp_relax_fcf_workspace")
 
 
+N_PARTS = 7   # translation units of csrc/mgrit_phi.cu (MGP_PART, see the .cu)
+
+
 def build(verbose: bool = False) -> str:
-    """Compile libmgrit_phi.so for sm_100a with nvcc (no GPU needed)."""
+    """Compile libmgrit_phi.so for sm_100a with nvcc (no GPU needed): the
+    source's N_PARTS kernel groups compile in parallel (-DMGP_PART=k, one
+    process each), then one link.  MGP_BUILD_PARTS=0 compiles it as a single
+    unit instead (same kernels, same flags)."""
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(_ROOT, "include"),
-           "-o", LIB_PATH, SRC_PATH]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+    extra = ["-Xptxas=-v"] if verbose else []
     if os.environ.get("MGP_FAST_BUILD") == "1":
         # development builds: nvcc splits the optimiser over all host cores
-        # (~4x faster; the SASS schedule differs slightly from the release build)
-        cmd.insert(1, "-split-compile=0")
-    subprocess.run(cmd, check=True)
+        # (faster; the SASS schedule differs from the release build)
+        extra.append("-split-compile=0")
+    inc = ["-I", os.path.join(_ROOT, "include")]
+    if os.environ.get("MGP_BUILD_PARTS", "1") == "0":
+        subprocess.run([nvcc, *extra, *NVCC_FLAGS, *inc, "-o", LIB_PATH, SRC_PATH], check=True)
+        return LIB_PATH
+    obj_dir = os.path.join(_PKG, "build")
+    os.makedirs(obj_dir, exist_ok=True)
+    # each unit's fatbin compressed like the single-unit build's (nvcc leaves
+    # smaller fatbins uncompressed by default)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-Xfatbin=-compress-all"]
+    objs, procs = [], []
+    for k in range(1, N_PARTS + 1):
+        obj = os.path.join(obj_dir, f"mgrit_phi.part{k}.o")
+        objs.append(obj)
+        procs.append(subprocess.Popen([nvcc, *extra, *compile_flags, *inc, f"-DMGP_PART={k}",
+                                       "-c", "-o", obj, SRC_PATH]))
+    bad = [k + 1 for k, pr in enumerate(procs) if pr.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, f"nvcc (MGP_PART {bad})")
+    subprocess.run([nvcc, "-shared", "-Xcompiler", "-fPIC", "-o", LIB_PATH, *objs], check=True)
     return LIB_PATH
 
 

@@ -107,7 +107,21 @@ __device__ __forceinline__ constexpr double tab_sm(int k, int s, int a, int b) {
 #define SM(k, s, a, b) c_sm[k][s][a][b]
 #endif
 
-namespace {
+namespace mgp_parts {
+extern unsigned long long launches;
+}
+
+// Translation-unit split (see the end of the file): every compilation gets
+// its own namespace for the internal code -- nvcc names an anonymous
+// namespace after the source file, so identical units would collide.
+#ifndef MGP_PART
+#define MGP_PART 0
+#endif
+#define MGP_CAT2(a, b) a##b
+#define MGP_CAT(a, b) MGP_CAT2(a, b)
+#define MGP_UNIT MGP_CAT(mgp_unit_, MGP_PART)
+
+namespace MGP_UNIT {
 
 using mgp::SharedRcp;
 using mgp::div_shared;
@@ -117,7 +131,9 @@ constexpr int kMaxThreads = 512;
 constexpr int kMaxRun = 8;
 constexpr int64_t kMaxNx = (int64_t)kMaxThreads * kMaxRun;
 
-unsigned long long g_launches = 0;
+// one launch counter for the whole library, whichever translation unit
+// (MGP_PART, below) the launch sits in
+unsigned long long &g_launches = mgp_parts::launches;
 #ifdef MGP_FCF_TRACE
 __device__ unsigned long long g_fcf_trace[4 * 8192];
 #endif
@@ -2272,18 +2288,32 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
 #endif
 }
 
-template <int MODEL>
+// KSET selects the instantiated kernels (translation-unit split, below):
+// bit 0 K = 0, bit 1 K = 1, bit 2 K = 2 sequential sums, bit 3 K = 2
+// two-lane sums, bit 4 K = 3
+constexpr int kKAll = 31;
+template <int MODEL, int KSET = kKAll>
 int launch_m(const mgp_sweep_args &a, cudaStream_t st) {
     const int reg = a.n_steps > 0 ? a.phi.regime : a.tail_regime;
     switch (a.phi.weno_k) {
-        case 0: return launch_p<0, MGP_SUM_SEQ, MODEL>(a, st);
-        case 1: return launch_p<1, MGP_SUM_SEQ, MODEL>(a, st);
+        case 0:
+            if constexpr ((KSET & 1) != 0) return launch_p<0, MGP_SUM_SEQ, MODEL>(a, st);
+            break;
+        case 1:
+            if constexpr ((KSET & 2) != 0) return launch_p<1, MGP_SUM_SEQ, MODEL>(a, st);
+            break;
         case 2:
-            return reg == MGP_SUM_SEQ ? launch_p<2, MGP_SUM_SEQ, MODEL>(a, st)
-                                      : launch_p<2, MGP_SUM_LANE2, MODEL>(a, st);
+            if (reg == MGP_SUM_SEQ) {
+                if constexpr ((KSET & 4) != 0) return launch_p<2, MGP_SUM_SEQ, MODEL>(a, st);
+            } else {
+                if constexpr ((KSET & 8) != 0) return launch_p<2, MGP_SUM_LANE2, MODEL>(a, st);
+            }
+            break;
         case 3:
-            return reg == MGP_SUM_SEQ ? launch_p<3, MGP_SUM_SEQ, MODEL>(a, st)
-                                      : launch_p<3, MGP_SUM_LANE2, MODEL>(a, st);
+            if constexpr ((KSET & 16) != 0)
+                return reg == MGP_SUM_SEQ ? launch_p<3, MGP_SUM_SEQ, MODEL>(a, st)
+                                          : launch_p<3, MGP_SUM_LANE2, MODEL>(a, st);
+            break;
     }
     return MGP_EINVAL;
 }
@@ -2342,6 +2372,9 @@ int launch_sys_k(const mgp_sweep_args &a, cudaStream_t st) {
     return MGP_EINVAL;
 }
 
+// a template so that only the translation unit that calls it instantiates
+// the system kernels
+template <int UNUSED = 0>
 int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
     const bool roe = a.phi.scheme == MGP_SCHEME_RK_WENO_ROE;
     if (a.phi.model == MGP_MODEL_EULER)
@@ -2535,8 +2568,61 @@ int validate(const mgp_sweep_args *a) {
     return MGP_OK;
 }
 
-}  // namespace
+}  // namespace MGP_UNIT
 
+using namespace MGP_UNIT;
+
+// ---- translation-unit split ------------------------------------------------
+// The library is built from MGP_NPARTS compilations of this file, run in
+// parallel (MGP_PART = 1..7; undefined = everything in one unit).  Each part
+// instantiates one group of kernels behind an externally visible entry;
+// part 1 also holds the C ABI, the fused FCF relaxation and the one-step LF
+// family.  Same code, flags and per-kernel compilation either way.
+#define MGP_IN_PART(n) (MGP_PART == 0 || MGP_PART == (n))
+
+namespace mgp_parts {
+int sweep_burgers_k2seq(const mgp_sweep_args &a, cudaStream_t st);
+int sweep_burgers_k2lane2(const mgp_sweep_args &a, cudaStream_t st);
+int sweep_burgers_k013(const mgp_sweep_args &a, cudaStream_t st);
+int sweep_roe(const mgp_sweep_args &a, cudaStream_t st);
+int sweep_advection(const mgp_sweep_args &a, cudaStream_t st);
+int sweep_systems(const mgp_sweep_args &a, cudaStream_t st);
+#if MGP_IN_PART(1)
+unsigned long long launches = 0;
+#endif
+#ifndef MGP_QUICK   // experiment builds: Burgers K = 2 through launch_m directly
+#if MGP_IN_PART(2)
+int sweep_burgers_k2seq(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_m<MGP_MODEL_BURGERS, 4>(a, st);
+}
+#endif
+#if MGP_IN_PART(3)
+int sweep_burgers_k2lane2(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_m<MGP_MODEL_BURGERS, 8>(a, st);
+}
+#endif
+#if MGP_IN_PART(4)
+int sweep_burgers_k013(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_m<MGP_MODEL_BURGERS, 1 | 2 | 16>(a, st);
+}
+#endif
+#if MGP_IN_PART(5)
+int sweep_roe(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_m<kModelBurgersRoe>(a, st);
+}
+#endif
+#if MGP_IN_PART(6)
+int sweep_advection(const mgp_sweep_args &a, cudaStream_t st) {
+    return launch_m<MGP_MODEL_ADVECTION>(a, st);
+}
+#endif
+#if MGP_IN_PART(7)
+int sweep_systems(const mgp_sweep_args &a, cudaStream_t st) { return launch_sys<>(a, st); }
+#endif
+#endif  // MGP_QUICK
+}  // namespace mgp_parts
+
+#if MGP_IN_PART(1)
 extern "C" {
 
 int mgp_sweep(const mgp_sweep_args *args, void *stream) {
@@ -2550,13 +2636,19 @@ int mgp_sweep(const mgp_sweep_args *args, void *stream) {
         return MGP_EINVAL;
     return launch_m<MGP_MODEL_BURGERS>(*args, st);
 #else
-    if (args->phi.model == MGP_MODEL_SHALLOW_WATER || args->phi.model == MGP_MODEL_EULER)
-        return launch_sys(*args, st);
-    if (args->phi.scheme == MGP_SCHEME_RK_WENO_ROE) return launch_m<kModelBurgersRoe>(*args, st);
-    if (args->phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(*args, st);
-    if (args->phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(*args, st);
-    if (args->phi.model == MGP_MODEL_BURGERS) return launch_m<MGP_MODEL_BURGERS>(*args, st);
-    return launch_m<MGP_MODEL_ADVECTION>(*args, st);
+    const mgp_sweep_args &a = *args;
+    if (a.phi.model == MGP_MODEL_SHALLOW_WATER || a.phi.model == MGP_MODEL_EULER)
+        return mgp_parts::sweep_systems(a, st);
+    if (a.phi.scheme == MGP_SCHEME_RK_WENO_ROE) return mgp_parts::sweep_roe(a, st);
+    if (a.phi.scheme == MGP_SCHEME_LF_ONESTEP) return launch_lf<1>(a, st);
+    if (a.phi.scheme == MGP_SCHEME_LF_MATCHED) return launch_lf<2>(a, st);
+    if (a.phi.model == MGP_MODEL_BURGERS) {
+        if (a.phi.weno_k != 2) return mgp_parts::sweep_burgers_k013(a, st);
+        const int reg = a.n_steps > 0 ? a.phi.regime : a.tail_regime;
+        return reg == MGP_SUM_SEQ ? mgp_parts::sweep_burgers_k2seq(a, st)
+                                  : mgp_parts::sweep_burgers_k2lane2(a, st);
+    }
+    return mgp_parts::sweep_advection(a, st);
 #endif
 }
 
@@ -2646,3 +2738,4 @@ int32_t mgp_sweep_args_layout(int64_t *out, int32_t n) {
 }
 
 }  // extern "C"
+#endif  // MGP_IN_PART(1)
