@@ -132,3 +132,31 @@ def test_workspace_query_and_rejections():
     with pytest.raises(P.ConfigError):
         dev.relax_fcf(phi, n_chunks=1024, m=4, g_mode=1, cs=c, cd=c.clone(),
                       workspace=ws[: nb // 2])           # workspace too small
+
+
+@pytest.mark.parametrize("window", ["1", "7", "192", "0"])
+def test_relax_to_host_zero_copy_ordered_loads(window):
+    """Zero-copy input: chain-start loads in ticket order with a bounded
+    window (MGP_FCF_ORDERED, read per launch; 0 = unordered) -- any window,
+    split or segment plan, gives the plain relaxation bit for bit."""
+    import os
+    pb = P.BASELINE_CONFIGS["c2"]
+    for segment, split in ((0, 0), (0, -1), (2, 0)):
+        fused, plain = _pair(pb, segment, split)
+        c_host = fused.c_points().reshape(-1, pb.n_x).cpu().pin_memory()
+        out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
+        old = os.environ.get("MGP_FCF_ORDERED")
+        os.environ["MGP_FCF_ORDERED"] = window
+        try:
+            for _ in range(2):                  # workspace counters reset by the launch
+                fused.relax_to_host(c_host, out, pieces=0)
+                torch.cuda.synchronize()
+                plain.load_c_points(c_host)
+                plain.relax(0)
+                assert torch.equal(out, plain.fine_values().cpu()), (window, segment, split)
+                c_host = fused.c_points().reshape(-1, pb.n_x).cpu().pin_memory()
+        finally:
+            if old is None:
+                os.environ.pop("MGP_FCF_ORDERED", None)
+            else:
+                os.environ["MGP_FCF_ORDERED"] = old
