@@ -31,6 +31,9 @@ for name in sys.argv[1:]:
     # the FCF workspace) stay out of the timed relaxation
     w = P.MgritHierarchy(st, u0, tg, pb.space_grid(), pb.options())
     w.relax(0)
+    if pb.n_x * pb.n_t <= 1 << 26:   # small configs: also load every kernel of a cycle
+        w.run_cycle()
+        w.monitor()
     torch.cuda.synchronize()
     del w
     # relaxation on finite data (the initial iterate): FCF on level 0
