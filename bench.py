@@ -3,22 +3,28 @@
 fine space-time point-updates/s of the WENO5 + SSP-RK3 propagator in MGRIT
 relaxation; s/iter).
 
-Workload (BASELINE.json configs[1], "c2"): 1D Burgers, N_x = 512, N_t = 4096,
-CFL 0.4, WENO5-JS (eps 1e-6) + global LF + SSP-RK3, fp64, seeded 4-mode
-Fourier IC (seed 1234), m = 4, FCF relaxation.  One step = one complete FCF
-relaxation of the finest level over all 1024 CF-intervals, F-points written
-to HBM: (2m - 1) * N_t/m * N_x = 3,670,016 point-updates, exactly the
-propagator applications the reference's relax(0) performs (mgrit.py:193-197).
+Workload (default, BASELINE.json configs[2], "c3" -- the largest
+single-GPU configuration): 1D Burgers, N_x = 4096, N_t = 65536, CFL 0.4,
+WENO5-JS (eps 1e-6) + global LF + SSP-RK3, fp64, seeded 8-mode Fourier IC
+(seed 1234), m = 4, 7 levels, FCF relaxation.  One step = one complete FCF
+relaxation of the finest level over all 16384 CF-intervals, F-points
+written to HBM: (2m - 1) * N_t/m * N_x = 469,762,048 point-updates, exactly
+the propagator applications of the reference's relax(0) (mgrit.py:193-197).
 The input iterate is the serial solution's C-points (finite data); each step
-relaxes the previous step's output.  L2 (126 MB) is flushed between steps
-(outside the timed region).  ``iteration_ms`` additionally times one whole
-V-cycle iteration + residual row of the same config from its initial
-iterate (the reference's MGRIT iteration 1; the config diverges there).
+relaxes the previous step's output.  The 126 MB L2 is flushed between steps
+(outside the timed region; the step's own input, 537 MB of C-points, is
+larger than L2 anyway).  ``iteration_ms`` times one whole V-cycle iteration
++ residual row of the same config from its initial iterate (the reference's
+MGRIT iteration 1, mgrit.py:315-332).  ``--workload c2`` keeps round 1's
+configs[1] line.
 
 ``--impl reference`` times the CPU oracle port (oracle/, a bit-exact C
-restatement of the reference propagator, all host threads) on the same
-relaxation -- the reference itself is Python/NumPy and is not installable
-on the GPU box.
+restatement of the reference propagator and MGRIT driver, all host threads):
+each step is a bounded sample -- the FCF relaxation of the first 1024
+CF-intervals of the same finest level (29.4 M point-updates) -- and
+``iteration_ms`` is one whole V-cycle + residual row of the full config,
+timed once.  The reference itself is Python/NumPy and is not installable on
+the GPU box.
 """
 from __future__ import annotations
 
@@ -52,7 +58,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c3", choices=["c2", "c3", "c4"])
+    ap.add_argument("--no-cpu-iteration", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
@@ -118,7 +125,15 @@ class ClockSampler:
 # CPU arm (oracle port)
 # ---------------------------------------------------------------------------
 
+CPU_SAMPLE_INTERVALS = 1024
+
+
 def cpu_relax_setup(pb):
+    """The oracle port on a bounded sample of the workload: a 2-level
+    hierarchy over the first CPU_SAMPLE_INTERVALS CF-intervals of the
+    finest level, holding the serial trajectory there (finite data, as the
+    GPU arm); its relax(0) is the reference's FCF relaxation of those
+    intervals (mgrit.py:193-197)."""
     import oracle
     from oracle import mgrit_oracle
     u0 = pb.initial_state()
@@ -128,17 +143,15 @@ def cpu_relax_setup(pb):
     st = oracle.OracleStepper(model=p["model"], k=p["k"], rk_order=p["rk_order"],
                               dt=p["dt"], dx=p["dx"], eps=p["eps"], speed=p["speed"],
                               nthreads=nthreads)
-    h = mgrit_oracle.Hierarchy([st] * pb.n_levels, u0, pb.n_t, tg.dt,
-                               mgrit_oracle.Options(n_levels=pb.n_levels, m=pb.m,
-                                                    relaxation="fcf"))
-    # start from the serial trajectory (finite data), as the GPU arm does
-    h.levels[0].u[:] = mgrit_oracle.march(st, u0, pb.n_t)
-    return h, nthreads
+    nci = min(CPU_SAMPLE_INTERVALS, pb.n_t // pb.m)
+    h = mgrit_oracle.Hierarchy([st, st], u0, nci * pb.m, tg.dt,
+                               mgrit_oracle.Options(n_levels=2, m=pb.m, relaxation="fcf"))
+    h.levels[0].u[:] = mgrit_oracle.march(st, u0, nci * pb.m)
+    return h, nthreads, (2 * pb.m - 1) * nci * pb.n_x, nci
 
 
 def cpu_relax_rate(pb, seconds: float):
-    h, nthreads = cpu_relax_setup(pb)
-    units = relax_units(pb)
+    h, nthreads, units, _ = cpu_relax_setup(pb)
     done, t0 = 0, time.perf_counter()
     while True:
         h.relax(0)
@@ -149,13 +162,38 @@ def cpu_relax_rate(pb, seconds: float):
     return units * done / el, nthreads, done, el
 
 
+def cpu_iteration_ms(pb):
+    """One whole MGRIT iteration of the full config on the oracle port
+    (run_cycle + residual_norm from the initial iterate, mgrit.py:315-322),
+    the CPU side of ``iteration_ms``."""
+    import oracle
+    from oracle import mgrit_oracle
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    nthreads = oracle.lib().ora_max_threads()
+    st = []
+    for l in range(pb.n_levels):
+        p = pb.phi_params(l)
+        st.append(oracle.OracleStepper(model=p["model"], k=p["k"], rk_order=p["rk_order"],
+                                       dt=p["dt"], dx=p["dx"], eps=p["eps"],
+                                       speed=p["speed"], nthreads=nthreads))
+    h = mgrit_oracle.Hierarchy(st, u0, pb.n_t, tg.dt,
+                               mgrit_oracle.Options(n_levels=pb.n_levels, m=pb.m,
+                                                    relaxation=pb.relaxation))
+    with np.errstate(all="ignore"):
+        t0 = time.perf_counter()
+        h.run_cycle()
+        r = h.residual_norm()
+        el = time.perf_counter() - t0
+    return 1e3 * el, r, nthreads
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     pb = workload(args.workload)
-    h, nthreads = cpu_relax_setup(pb)
-    units = relax_units(pb)
+    h, nthreads, units, nci = cpu_relax_setup(pb)
     for _ in range(args.warmup):
         h.relax(0)
     times = []
@@ -165,8 +203,9 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = units * args.steps / total
-    sample = (f"{args.steps} full FCF relaxations of the finest level "
-              f"({units} point-updates each), oracle C port, {nthreads} threads")
+    sample = (f"per step: FCF relaxation of the first {nci} of {pb.n_t // pb.m} "
+              f"CF-intervals of the finest level ({units} point-updates), "
+              f"oracle C port, {nthreads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -178,6 +217,12 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu_iteration:
+        it_ms, r, _ = cpu_iteration_ms(pb)
+        line["iteration_ms"] = it_ms
+        line["iteration_note"] = (f"one whole V-cycle ({pb.n_levels} levels, FCF) + residual "
+                                  f"row of the full config from the initial iterate, oracle "
+                                  f"port, {nthreads} threads (residual after: {r})")
     print(json.dumps(line), flush=True)
 
 
@@ -189,7 +234,8 @@ def config_block(pb, args):
             "step": "one FCF relaxation of the finest level, all CF-intervals, "
                     "F-points stored",
             "point_updates_per_step": relax_units(pb),
-            "l2": "flushed (256 MiB write) between timed steps"}
+            "l2": "flushed (256 MiB write) between timed steps",
+            "input": "serial solution's C-points (finite data), resident in HBM"}
 
 
 # ---------------------------------------------------------------------------
@@ -440,17 +486,20 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clock_info,
         "iteration_ms": statistics.median(it_ms),
-        "iteration_note": "one V-cycle (FCF, 2 levels, 1024-step sequential coarse solve) "
-                          "+ residual row from the initial iterate; config diverges in it. 1 "
+        "iteration_note": f"one V-cycle (FCF, {pb.n_levels} levels, "
+                          f"{pb.n_t // pb.m ** (pb.n_levels - 1)}-step sequential coarse solve) "
+                          "+ residual row from the initial iterate, median of 3 "
                           f"(residual after: {mon.residual})",
         "kernel_ms": ({"fcf": statistics.median(k_fc)} if fused else
                       {"fused_f_c": statistics.median(k_fc), "f_store": statistics.median(k_f)}),
     }
     if not args.no_cpu_baseline and world == 1:
         rate, cores, n, el = cpu_relax_rate(pb, args.cpu_seconds)
+        nci = min(CPU_SAMPLE_INTERVALS, nc)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                                "sample": f"{n} full FCF relaxation(s) of the same workload "
-                                          f"in {el:.1f} s (oracle C port)"}
+                                "sample": f"{n} FCF relaxation(s) of the first {nci} of {nc} "
+                                          f"CF-intervals of the same finest level in "
+                                          f"{el:.1f} s (oracle C port)"}
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()

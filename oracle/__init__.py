@@ -60,6 +60,45 @@ class OraParams(ctypes.Structure):
 
 
 _lib = None
+REF_DIR = os.path.join(_HERE, "_ref")
+REFERENCE_PKG = "/root/reference/pkg"
+
+
+def install_reference(force: bool = False) -> str | None:
+    """Install the UNMODIFIED reference package (mgritlab, pure Python) into
+    ``oracle/_ref`` -- a pip install from a /tmp copy of its sources (the
+    source tree is read-only), no dependencies (NumPy is in the image).
+    git-ignored, but shipped to the GPU box with the repo snapshot, where the
+    drop-in tests run the reference's own ``mgrit_solve`` with the GPU
+    steppers.  Returns the install directory, or None when the reference
+    sources are absent (the GPU box)."""
+    import shutil
+    import sys
+    import tempfile
+    if os.path.isdir(os.path.join(REF_DIR, "mgritlab")) and not force:
+        return REF_DIR
+    if not os.path.isdir(REFERENCE_PKG):
+        return None
+    with tempfile.TemporaryDirectory() as tmp:
+        src = os.path.join(tmp, "pkg")
+        shutil.copytree(REFERENCE_PKG, src)
+        shutil.rmtree(REF_DIR, ignore_errors=True)
+        subprocess.run([sys.executable, "-m", "pip", "install", "--quiet", "--no-index",
+                        "--no-build-isolation", "--no-deps", "--target", REF_DIR, src],
+                       check=True)
+    return REF_DIR
+
+
+def import_reference():
+    """The installed reference package (``import mgritlab`` from oracle/_ref),
+    or None if it was not installed."""
+    import importlib
+    import sys
+    if not os.path.isdir(os.path.join(REF_DIR, "mgritlab")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    return importlib.import_module("mgritlab")
 
 
 def build(force: bool = False) -> str:

@@ -174,8 +174,20 @@ def march(stepper, u0, n_steps):
 
 
 def mgrit_solve(steppers, u0, n_steps, dt0, opts: Options, reference=None,
-                hierarchy_out: list | None = None):
-    """mgrit.py:276-340 (without the thread pool: parallelism=1 semantics)."""
+                hierarchy_out: list | None = None, residual_tol: float | None = None,
+                on_row=None):
+    """mgrit.py:276-340 (without the thread pool: parallelism=1 semantics).
+
+    A PhysicalStateError raised inside a cycle is recorded as divergence at
+    that iteration (mgrit.py:316-320); one raised by the monitoring that
+    follows the cycle propagates, as in the reference (mgrit.py:321-322 call
+    residual_norm outside the try).  The oracle's stand-in exception is
+    ``oracle.PhysicalStateOracleError``.  ``residual_tol`` (the package's
+    BASELINE-config-1 extension) stops after the first row whose residual is
+    below it (rows >= 1, as the package's driver): the rows are a prefix of
+    the reference's.  ``on_row(it, h)`` is
+    called after every recorded row (fixture hashing)."""
+    from . import PhysicalStateOracleError
     h = Hierarchy(steppers, u0, n_steps, dt0, opts)
     if hierarchy_out is not None:
         hierarchy_out.append(h)
@@ -194,8 +206,16 @@ def mgrit_solve(steppers, u0, n_steps, dt0, opts: Options, reference=None,
     with np.errstate(all="ignore"):
         errors[0] = err()
         resid[0] = h.residual_norm()
+        if on_row is not None:
+            on_row(0, h)
         for it in range(1, rows):
-            h.run_cycle()
+            if residual_tol is not None and it >= 2 and resid[it - 1] < residual_tol:
+                break
+            try:
+                h.run_cycle()
+            except PhysicalStateOracleError:
+                diverged, at = True, it
+                break
             e = err()
             r = h.residual_norm()
             finite = bool(np.all(np.isfinite(h.fine_values())))
@@ -207,4 +227,6 @@ def mgrit_solve(steppers, u0, n_steps, dt0, opts: Options, reference=None,
                 break
             errors[it] = e
             resid[it] = r
+            if on_row is not None:
+                on_row(it, h)
     return h.fine_values(), Record(errors, resid, diverged, at)

@@ -196,5 +196,26 @@ def max_nx_static(weno_k: int = 2, model: int = 0) -> int:
     return 16 * 4096 if (weno_k == 2 and model == MODEL_BURGERS) else 4096
 
 
+CTA_MAX_NX = 4096
+
+
+def split_cluster_size(nx: int) -> int:
+    """Cluster size the library splits a mesh of nx > 4096 cells over: the
+    smallest cs in {2, 4, 8, 16} with nx % cs == 0 and nx / cs <= 4096, or 0
+    if none exists (mgp_sweep then returns MGP_EINVAL) -- csrc split_cs."""
+    for cs in (2, 4, 8, 16):
+        if nx % cs == 0 and nx // cs <= CTA_MAX_NX:
+            return cs
+    return 0
+
+
+def mesh_supported(nx: int, weno_k: int = 2, model: int = 0) -> bool:
+    """nx within the kernel's limit and, above one CTA's 4096 cells, split
+    evenly into power-of-two slabs (csrc validate())."""
+    if nx > max_nx_static(weno_k, model):
+        return False
+    return nx <= CTA_MAX_NX or split_cluster_size(nx) > 0
+
+
 def max_nx(weno_k: int = 2, model: int = 0) -> int:
     return int(load().mgp_max_nx(int(weno_k), int(model)))

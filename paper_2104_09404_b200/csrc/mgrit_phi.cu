@@ -1223,6 +1223,25 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
 
 Consts make_consts(const mgp_phi &p);
 
+// Kernel attributes (dynamic shared memory above 48 KB, 16-CTA clusters) are
+// per device context: one flag bit per device index, set on first use there.
+template <class Kern>
+bool ensure_attrs(Kern kern, unsigned long long &devs, bool nonportable_cluster) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (devs & bit) return true;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+        cudaSuccess)
+        return false;
+    if (nonportable_cluster &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess)
+        return false;
+    devs |= bit;
+    return true;
+}
+
 template <int K, int REG, int CS>
 int launch_march(const mgp_sweep_args &a, cudaStream_t st) {
     const int ns = (int)(a.phi.nx / CS);
@@ -1231,16 +1250,8 @@ int launch_march(const mgp_sweep_args &a, cudaStream_t st) {
     const size_t sm = sizeof(double) * (size_t)(2 * (ns + 2 * G) + 4 * (ns + 2 * G + 1)) +
                       sizeof(unsigned long long) * (size_t)(2 * CS * (nt / 32));
     auto kern = march_kernel<K, REG, CS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024) != cudaSuccess)
-            return MGP_ECUDA;
-        if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                           1) != cudaSuccess)
-            return MGP_ECUDA;
-        attr_set = true;
-    }
+    static unsigned long long attr_devs = 0;
+    if (!ensure_attrs(kern, attr_devs, CS > 8)) return MGP_ECUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)CS);
     cfg.blockDim = dim3(nt);
@@ -2131,16 +2142,8 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     const int nt = threads_for(ns, P);
     const size_t sm = smem_bytes(ns, K, CS);
     auto kern = sweep_kernel<K, REG, MODEL, P, REGS, CS>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024) != cudaSuccess)
-            return MGP_ECUDA;
-        if (CS > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                           1) != cudaSuccess)
-            return MGP_ECUDA;
-        attr_set = true;
-    }
+    static unsigned long long attr_devs = 0;
+    if (!ensure_attrs(kern, attr_devs, CS > 8)) return MGP_ECUDA;
     int64_t grid = a.n_chunks;
     if (grid > ((int64_t)1 << 30) / CS) grid = ((int64_t)1 << 30) / CS;
     const Consts k = make_consts(a.phi);
@@ -2177,15 +2180,19 @@ int env_int(const char *name) {
 // Cluster size for a field: meshes above one SM's capacity must be split
 // (WENO5 Burgers only, up to 16 x 4096 cells); single-field marches of the
 // sequential coarse solve are split for latency (MGP_MARCH_CS overrides).
+// Smallest cluster size cs in {2, 4, 8, 16} that splits a mesh of nx > kMaxNx
+// cells into equal slabs of at most kMaxNx cells, or 0 if none does.
+int split_cs(int64_t nx) {
+    for (int cs = 2; cs <= 16; cs *= 2)
+        if (nx % cs == 0 && nx / cs <= kMaxNx) return cs;
+    return 0;
+}
+
 int cluster_size(const mgp_sweep_args &a) {
     const int64_t nx = a.phi.nx;
     const bool cl_ok = a.phi.weno_k == 2 && a.phi.model == MGP_MODEL_BURGERS &&
                        a.phi.scheme == MGP_SCHEME_RK_WENO;
-    if (nx > kMaxNx) {
-        int cs = 2;
-        while (nx / cs > kMaxNx || nx % cs) cs *= 2;
-        return cs;
-    }
+    if (nx > kMaxNx) return split_cs(nx);   // validate() guarantees a size exists
     if (cl_ok && a.n_chunks == 1) {
         const int env = env_int("MGP_MARCH_CS");   // per call (tests switch it)
         // default: slabs of >= 64 cells, at most 16 CTAs (measured, latency
@@ -2346,13 +2353,8 @@ int launch_lf(const mgp_sweep_args &a, cudaStream_t st) {
     if (nt > 256) nt = 256;
     const size_t sm = sizeof(double) * (size_t)(7 * nx + 3 * 32 + 3);
     auto kern = lf_kernel<MODE>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024) != cudaSuccess)
-            return MGP_ECUDA;
-        attr_set = true;
-    }
+    static unsigned long long attr_devs = 0;
+    if (!ensure_attrs(kern, attr_devs, false)) return MGP_ECUDA;
     int64_t grid = a.n_chunks;
     if (grid > (int64_t)1 << 30) grid = (int64_t)1 << 30;
     kern<<<(unsigned)grid, nt, sm, st>>>(a, make_consts(a.phi));
@@ -2368,13 +2370,8 @@ int launch_sys_t(const mgp_sweep_args &a, cudaStream_t st) {
     const size_t sm = sizeof(double) * (size_t)(D * (nx + 2 * K) + 3 * D * nx + 3 * 32 + 3) +
                       sizeof(unsigned long long) * 32;
     auto kern = sys_kernel<K, ROE, D>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024) != cudaSuccess)
-            return MGP_ECUDA;
-        attr_set = true;
-    }
+    static unsigned long long attr_devs = 0;
+    if (!ensure_attrs(kern, attr_devs, false)) return MGP_ECUDA;
     int64_t grid = a.n_chunks;
     if (grid > (int64_t)1 << 30) grid = (int64_t)1 << 30;
     kern<<<(unsigned)grid, nt, sm, st>>>(a, make_consts(a.phi));
@@ -2416,13 +2413,8 @@ int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
     const int ns = (int)phi.nx;
     L.nt = threads_for(ns, P);
     L.smem = smem_bytes(ns, K, 1);
-    static bool attr_set = false;
-    if (!attr_set) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024) != cudaSuccess)
-            return MGP_ECUDA;
-        attr_set = true;
-    }
+    static unsigned long long attr_devs = 0;
+    if (!ensure_attrs(kern, attr_devs, false)) return MGP_ECUDA;
     int dev = 0, nsm = 0, per = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
@@ -2571,14 +2563,8 @@ int validate(const mgp_sweep_args *a) {
     if (p.rk_order < 0 || p.rk_order > 3) return MGP_EINVAL;
     if (p.regime != MGP_SUM_SEQ && p.regime != MGP_SUM_LANE2) return MGP_EINVAL;
     if (p.nx < 2 * p.weno_k + 1 || p.nx > max_nx_for(p.weno_k, p.model)) return MGP_EINVAL;
-    if (!system && p.nx > kMaxNx &&
-        p.nx % (((p.nx + kMaxNx - 1) / kMaxNx + 0)) != 0) {
-        int cs = 2;
-        while (p.nx / cs > kMaxNx || p.nx % cs) {
-            cs *= 2;
-            if (cs > 16) return MGP_EINVAL;
-        }
-    }
+    // meshes above one CTA's capacity: equal power-of-two slabs of <= kMaxNx
+    if (!system && p.nx > kMaxNx && split_cs(p.nx) == 0) return MGP_EINVAL;
     if (!(p.dx > 0.0) || !(p.epsilon > 0.0)) return MGP_EINVAL;
     if (a->n_chunks < 0 || a->n_steps < 0 || !a->start) return MGP_EINVAL;
     if (a->g_mode < MGP_G_NONE || a->g_mode > MGP_G_ARRAY) return MGP_EINVAL;

@@ -112,6 +112,31 @@ def raise_for_status(v: int) -> None:
                                  + "; ".join(what))
 
 
+def snapshot_status() -> torch.Tensor:
+    """Move the status word's bits into a new device tensor and clear the
+    word, in stream order (no synchronisation): the bits the work enqueued
+    so far set, separated from those of later work."""
+    w = status_word()
+    snap = w.clone()
+    w.zero_()
+    return snap
+
+
+STATUS_BITS = (STATUS_NONPOSITIVE_DEPTH, STATUS_NONPOSITIVE_DENSITY,
+               STATUS_NONPOSITIVE_PRESSURE, STATUS_ROE_NONHYPERBOLIC)
+
+
+def status_to_bits(word: torch.Tensor) -> torch.Tensor:
+    """int32 status word -> one 0/1 entry per MGP_STATUS_* bit (a MAX
+    all-reduce of these is the bitwise OR of every rank's word)."""
+    masks = torch.tensor(STATUS_BITS, dtype=torch.int32, device=word.device)
+    return ((word.reshape(1) & masks) != 0).to(torch.int64)
+
+
+def bits_to_status(bits) -> int:
+    return sum(b for b, on in zip(STATUS_BITS, bits) if on)
+
+
 def check_status() -> None:
     """Raise PhysicalStateError if a sweep since the last check met a
     state the reference rejects."""

@@ -41,7 +41,7 @@ from ._lib import (G_ARRAY, G_ZERO, GUESS_INJECTION, GUESS_LAST_STEP, SUM_SEQ,
                    TAIL_PHI, TAIL_RESID, TAIL_RESTRICT)
 from .errors import ConfigError, DimensionError
 from .grid import SpatialGrid, TemporalGrid, Trajectory
-from .mgrit import ConvergenceRecord, Monitor, MgritOptions, _check_stepper
+from .mgrit import ConvergenceRecord, Monitor, MgritOptions, _check_stepper, _ref_norm_sq
 
 
 def partition(n_steps: int, m: int, n_levels: int, world: int):
@@ -475,28 +475,45 @@ def mgrit_solve_distributed(steppers, initial_state, time_grid, space_grid,
     ref = ref_norm = None
     if reference is not None:
         ref = dev.to_device(reference)
-        ref_norm = math.sqrt(float((ref.reshape(-1) * ref.reshape(-1)).sum().item()))
+        ref_norm = math.sqrt(_ref_norm_sq(ref, h.nx, h.steppers[0]))
+        if ref_norm == 0.0:
+            raise ValueError("reference trajectory has zero norm")
     rows = options.max_iters + 1
     errors = np.full(rows, np.nan)
     residuals = np.full(rows, np.nan)
     diverged, at = False, None
+    checked = h.n_components > 1     # systems: PhysicalStateError
 
     def error(mon):
         return math.nan if ref is None else math.sqrt(mon.error_sq) / ref_norm
 
-    def watch(mon):
-        # shallow water: every rank raises PhysicalStateError together
-        if h.n_components > 1:
-            flag = torch.tensor([dev.take_status()], dtype=torch.int64, device=h.device)
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-            dev.raise_for_status(int(flag.item()))
-        return mon
+    def status_bits(cycle_word):
+        """(cycle word, monitor word), each OR-ed over all ranks (a MAX
+        all-reduce of per-bit flags), so every rank decides together."""
+        mon_word = dev.snapshot_status()
+        cyc = dev.status_to_bits(cycle_word) if cycle_word is not None else \
+            torch.zeros(len(dev.STATUS_BITS), dtype=torch.int64, device=h.device)
+        flags = torch.cat([cyc, dev.status_to_bits(mon_word)])
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+        f = flags.cpu().tolist()
+        n = len(dev.STATUS_BITS)
+        return dev.bits_to_status(f[:n]), dev.bits_to_status(f[n:])
 
-    mon = watch(h.monitor(ref))
+    mon = h.monitor(ref)
+    if checked:
+        dev.raise_for_status(status_bits(None)[1])
     errors[0], residuals[0] = error(mon), mon.residual
     for it in range(1, rows):
         h.run_cycle()
-        mon = watch(h.monitor(ref))
+        cycle_word = dev.snapshot_status() if checked else None
+        mon = h.monitor(ref)
+        if checked:
+            # inside the cycle: recorded (mgrit.py:316-320); monitor: raised
+            cyc, after = status_bits(cycle_word)
+            if cyc:
+                diverged, at = True, it
+                break
+            dev.raise_for_status(after)
         err = error(mon)
         if mon.nonfinite != 0 or (np.isfinite(err) and err > options.divergence_threshold):
             diverged, at = True, it

@@ -78,6 +78,10 @@ class SemiDiscreteOperator:
         if space_grid.n_cells > dev._lib.max_nx_static(config.weno.degree, model.abi_model):
             raise ConfigError(f"{space_grid.n_cells} cells exceed the {kind} kernel's "
                               f"limit")
+        if not dev._lib.mesh_supported(space_grid.n_cells, config.weno.degree,
+                                       model.abi_model):
+            raise ConfigError(f"{space_grid.n_cells} cells cannot be split into 2, 4, 8 "
+                              f"or 16 equal slabs of at most {dev._lib.CTA_MAX_NX} cells")
         self.model = model
         self.space_grid = space_grid
         self.config = config

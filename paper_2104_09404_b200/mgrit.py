@@ -664,7 +664,7 @@ def _ref_norm_sq(reference: torch.Tensor, nx: int, stepper) -> float:
 def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
                 space_grid: SpatialGrid, options: MgritOptions, reference=None,
                 *, return_trajectory: bool = True, hierarchy_out: list | None = None,
-                residual_tol: float | None = None):
+                residual_tol: float | None = None, on_row=None):
     """Iterate cycles until max_iters, recording convergence per iteration
     (mgrit.py:276-340): row 0 is the initial iterate; divergence (non-finite
     iterate, or relative error above the threshold, or a non-finite error
@@ -676,7 +676,15 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     array (``return_trajectory=False`` skips materialising it, e.g. for
     problems whose full trajectory does not fit in memory).  residual_tol
     (not in the reference, BASELINE config 1 "stop at residual < 1e-10")
-    stops after the first row whose residual is below it.
+    stops after the first row whose residual is below it.  ``on_row(it, h)``
+    is called after every recorded row with the hierarchy (test hook).
+
+    Systems: a PhysicalStateError condition met inside a cycle is recorded
+    as divergence at that iteration (mgrit.py:316-320; the GPU finishes the
+    cycle on the inadmissible state instead of unwinding mid-cycle, so the
+    returned trajectory is the completed cycle's, not the reference's
+    partially updated arrays); met by row 0 or by the monitoring after a
+    cycle, it raises, as the reference's residual_norm() does.
     """
     h = MgritHierarchy(steppers, initial_state, time_grid, space_grid, options)
     if hierarchy_out is not None:
@@ -719,11 +727,23 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     mon = watch(h.monitor(ref))
     errors[0] = error(mon)
     residuals[0] = mon.residual
+    if on_row is not None:
+        on_row(0, h)
     for it in range(1, n_rows):
         if residual_tol is not None and converged_at is not None:
             break
         h.run_cycle()
-        mon = watch(h.monitor(ref))
+        # a state the reference rejects met INSIDE the cycle is recorded as
+        # divergence (mgrit.py:316-320); met by the monitoring that follows it
+        # raises, as the reference's residual_norm() does (mgrit.py:322).  The
+        # cycle's bits are split from the monitor's in stream order.
+        cycle_status = dev.snapshot_status() if checked else None
+        mon = h.monitor(ref)
+        if cycle_status is not None and int(cycle_status.item()):
+            dev.take_status()
+            diverged, diverged_at = True, it
+            break
+        mon = watch(mon)
         err = error(mon)
         finite = mon.nonfinite == 0
         if not finite or (np.isfinite(err) and err > options.divergence_threshold):
@@ -734,6 +754,8 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
             break
         errors[it] = err
         residuals[it] = mon.residual
+        if on_row is not None:
+            on_row(it, h)
         if residual_tol is not None and converged_at is None and mon.residual < residual_tol:
             converged_at = it
     record = ConvergenceRecord(errors=errors, residuals=residuals,

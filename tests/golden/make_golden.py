@@ -580,6 +580,106 @@ def sw_mgrit_cases():
 
 
 # ---------------------------------------------------------------------------
+# PhysicalStateError inside a cycle is recorded as divergence (mgrit.py:
+# 316-320); raised by the row-0 residual it propagates (mgrit.py:306-307).
+# Shallow-water variants of high_order_shallow_water_*.cfg with a longer
+# horizon / fewer steps, found with the reference (coarse CFL too large:
+# a depth goes non-positive inside V-cycle 1 or 2).
+# ---------------------------------------------------------------------------
+
+SW_DIVERGE = [
+    # (name, cfg, horizon, n_t, weno_order, expected outcome in the reference)
+    ("sw_psd_lf_T0.75_nt160_w5", "high_order_shallow_water_lf.cfg", 0.75, 160, 5),
+    ("sw_psd_lf_T0.75_nt160_w3", "high_order_shallow_water_lf.cfg", 0.75, 160, 3),
+    ("sw_psd_lf_T1.0_nt200_w1", "high_order_shallow_water_lf.cfg", 1.0, 200, 1),
+    ("sw_psd_roe_T1.0_nt200_w3", "high_order_shallow_water_roe.cfg", 1.0, 200, 3),
+    ("sw_psd_lf_T20_nt40_w1_row0", "high_order_shallow_water_lf.cfg", 20.0, 40, 1),
+]
+
+
+def sw_divergence_cases():
+    from mgritlab.errors import PhysicalStateError
+    from mgritlab.harness import build_steppers as ref_build_steppers
+    import mgritlab.mgrit as RM
+    arrays, meta = {}, []
+    cfg_dir = "/root/reference/pkg/configs"
+    for name, fname, horizon, n_t, order in SW_DIVERGE:
+        base = R.load_config(os.path.join(cfg_dir, fname))
+        col = dataclasses.replace(base, sweep=None, sweep_values=(), weno_order=(order,),
+                                  horizon=horizon, n_t=n_t, max_iters=4)
+        sg = R.SpatialGrid(col.length, col.n_x)
+        tg = R.TemporalGrid(col.horizon, col.n_t)
+        model = R.make_model(col.problem)
+        u0 = R.initial_state(col.ic, sg, col.length)
+        steppers = ref_build_steppers(col, model, sg, tg)
+        try:
+            reference = R.solve_serial(steppers[0], u0, tg, sg, model).trajectory.values
+        except PhysicalStateError:
+            reference = None
+        opts = R.MgritOptions(n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                              relaxation=col.relaxation, guess=col.restriction_guess,
+                              max_iters=col.max_iters)
+        # which cycle raised (the record only says diverged_at)
+        raised_in_cycle = []
+        orig = RM.MgritHierarchy.run_cycle
+
+        def run_cycle(self, _orig=orig):
+            try:
+                return _orig(self)
+            except PhysicalStateError:
+                raised_in_cycle.append(True)
+                raise
+        RM.MgritHierarchy.run_cycle = run_cycle
+        try:
+            _, rec = R.mgrit_solve(steppers, u0, tg, sg, opts, reference=reference)
+            outcome = "recorded"
+        except PhysicalStateError:
+            rec, outcome = None, "raises"
+        finally:
+            RM.MgritHierarchy.run_cycle = orig
+        ost = [oracle.OracleStepper(model="shallow-water", k=st.rhs.__self__.config.weno.degree,
+                                    rk_order=st.order, dt=st.dt, dx=sg.dx, eps=1e-6,
+                                    nthreads=1, gravity=model.gravity,
+                                    scheme=3 if col.flux == "roe" else 0)
+               for st in steppers]
+        o_opts = mgrit_oracle.Options(n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                                      relaxation=col.relaxation, guess=col.restriction_guess,
+                                      max_iters=col.max_iters)
+        if outcome == "raises":
+            try:
+                mgrit_oracle.mgrit_solve(ost, u0, col.n_t, tg.dt, o_opts)
+                raise AssertionError(name + ": oracle did not raise")
+            except oracle.PhysicalStateOracleError:
+                pass
+        else:
+            o_ref = None
+            if reference is not None:
+                o_ref = mgrit_oracle.march(ost[0], u0, col.n_t)
+                assert np.array_equal(o_ref, reference), name
+            _, orec = mgrit_oracle.mgrit_solve(ost, u0, col.n_t, tg.dt, o_opts,
+                                               reference=o_ref)
+            assert orec.diverged_at == rec.diverged_at, (name, orec.diverged_at)
+            ok = np.isfinite(rec.residuals)
+            assert np.allclose(orec.residuals[ok], rec.residuals[ok], rtol=1e-12), name
+            arrays[name + "__errors"] = rec.errors
+            arrays[name + "__residuals"] = rec.residuals
+        arrays[name + "__u0"] = u0
+        meta.append(dict(name=name, config=fname, model="shallow-water", n_x=col.n_x,
+                         n_t=col.n_t, horizon=col.horizon, length=col.length, flux=col.flux,
+                         stepper=list(col.stepper), weno_order=list(col.weno_order),
+                         coarse=col.coarse, n_levels=col.n_levels, m=col.m, cycle=col.cycle,
+                         relaxation=col.relaxation, guess=col.restriction_guess,
+                         max_iters=col.max_iters, gravity=model.gravity, ic=col.ic,
+                         has_reference=reference is not None, outcome=outcome,
+                         physical_state_error_in_cycle=bool(raised_in_cycle),
+                         diverged_at=None if rec is None else rec.diverged_at))
+        print(f"{name}: {outcome} diverged_at={None if rec is None else rec.diverged_at}")
+    np.savez_compressed(os.path.join(HERE, "sw_diverge_cases.npz"), **arrays)
+    with open(os.path.join(HERE, "sw_diverge_cases.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
+# ---------------------------------------------------------------------------
 # Euler (models.py:214-308) and componentwise systems -- SURVEY.md 8(f) rank 4
 #
 # The reference takes Euler's left eigenvectors with np.linalg.inv (LAPACK
@@ -794,6 +894,8 @@ if __name__ == "__main__":
     if "sw" in which:
         sw_vectors()
         sw_mgrit_cases()
+    if "sw" in which or "swdiv" in which:
+        sw_divergence_cases()
     if "phi" in which:
         phi_vectors()
     if "mgrit" in which:

@@ -1,0 +1,182 @@
+"""Full-size parity on the GPU, against oracle fixtures generated at the
+BASELINE configs' own sizes (tests/golden/make_golden_full.py) and against
+the oracle run live on the box's host cores.
+
+* BASELINE config 4: all 192 cases at N_x = 1024, N_t = 16384 -- identical
+  iterations to 1e-10, identical divergence iteration, residual rows within
+  1e-10 relative (exact zeros exact), and the finest iterate after EVERY
+  recorded row bit-identical (canonical SHA-256: NaNs as one pattern,
+  -0.0 as +0.0).
+* BASELINE config 5's mesh (N_x = 65536, m = 16, 16-mode a_k/k IC) with
+  N_t = 4096, L = 3: the config's own CFL and a converging variant.
+* The bench kernel (fused FCF relaxation, F-points stored,
+  ``relax_fine_values``) at the full config-2 and config-3 shapes vs the
+  oracle's ``Hierarchy.relax(0)`` (mgrit.py:193-197), from the serial
+  C-points and from a perturbed iterate.
+* Shallow water: a PhysicalStateError condition met inside V-cycle 1 or 2 is
+  recorded as divergence, met at row 0 it raises (mgrit.py:306-322),
+  against reference-generated fixtures (make_golden.py swdiv).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2104_09404_b200 as P
+from oracle import mgrit_oracle
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+from fixture_hash import canonical_hash
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+def _load(name):
+    path = os.path.join(GOLDEN, name)
+    if not os.path.exists(path):
+        return {}
+    return {c["name"]: c for c in json.load(open(path))["cases"]}
+
+
+C4 = _load("full_c4.json")
+C5 = _load("full_c5.json")
+
+
+def _problem(fx):
+    base = P.BASELINE_CONFIGS["c5" if fx["n_x"] == 65536 else "c4"]
+    return base.scaled(name=fx["name"], n_x=fx["n_x"], n_t=fx["n_t"], cfl=fx["cfl"],
+                       m=fx["m"], n_levels=fx["n_levels"], weno_order=tuple(fx["weno"]),
+                       stepper=tuple(fx["stepper"]), relaxation=fx["relaxation"],
+                       cycle=fx["cycle"], guess=fx["guess"], n_modes=fx["n_modes"],
+                       decay=fx["decay"], seed=fx["seed"], max_iters=fx["max_iters"])
+
+
+def _run_and_check(fx):
+    pb = _problem(fx)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    assert tg.dt == fx["dt"], fx["name"]
+    hashes = []
+    _, rec = P.mgrit_solve(
+        pb.steppers(tg), u0, tg, pb.space_grid(), pb.options(), return_trajectory=False,
+        residual_tol=fx["residual_tol"], hierarchy_out=(hout := []),
+        on_row=lambda it, h: hashes.append(canonical_hash(h.fine_values().cpu().numpy())))
+    name = fx["name"]
+    assert rec.diverged_at == fx["diverged_at"], name
+    assert rec.converged_at == fx["converged_at"], name
+    want = np.array([np.nan if r is None else r for r in fx["residuals"]])
+    got = rec.residuals[:len(want)]
+    ok = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), ok), name
+    np.testing.assert_allclose(got[ok], want[ok], rtol=RTOL, atol=0, err_msg=name)
+    assert np.array_equal(got[ok] == 0.0, want[ok] == 0.0), name
+    assert hashes == fx["iterate_sha256"], name
+    assert canonical_hash(hout[0].fine_values().cpu().numpy()) == fx["final_sha256"], name
+
+
+@pytest.mark.parametrize("name", sorted(C4))
+def test_c4_full_grid_case(name):
+    _run_and_check(C4[name])
+
+
+def test_c4_fixture_is_complete():
+    assert len(C4) == 192
+    conv = [c for c in C4.values() if c["converged_at"] is not None]
+    assert conv, "no converging config-4 case"
+
+
+@pytest.mark.parametrize("name", sorted(C5))
+def test_c5_mesh_case(name):
+    _run_and_check(C5[name])
+
+
+# ---------------------------------------------------------------------------
+# the bench kernel at full size against the oracle, live on the host cores
+# ---------------------------------------------------------------------------
+
+def _oracle_relax(pb, c_points):
+    p = pb.phi_params(0)
+    st = oracle.OracleStepper(model=p["model"], k=p["k"], rk_order=p["rk_order"], dt=p["dt"],
+                              dx=p["dx"], eps=p["eps"], speed=p["speed"], nthreads=0)
+    h = mgrit_oracle.Hierarchy([st, st], np.asarray(c_points[0])[None], pb.n_t, p["dt"],
+                               mgrit_oracle.Options(n_levels=2, m=pb.m, relaxation="fcf"))
+    h.levels[0].u[::pb.m, 0] = c_points      # F-points are overwritten by relax's F-relax
+    h.relax(0)
+    return h.levels[0].u
+
+
+@pytest.mark.parametrize("cfg,perturb", [("c2", False), ("c2", True), ("c3", True)])
+def test_bench_relaxation_full_size_vs_oracle(cfg, perturb):
+    pb = P.BASELINE_CONFIGS[cfg]
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    c = P.serial.march(steppers[0], u0, pb.n_t)[::pb.m, 0].cpu().numpy()
+    if perturb:      # not a fixed point: every interval's relaxation changes it
+        rng = np.random.default_rng(5)
+        c = c + 1e-3 * rng.standard_normal(c.shape)
+        c[0] = u0[0]
+    h = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    h.load_c_points(c)
+    got = h.relax_fine_values().cpu().numpy()[:, 0]
+    want = _oracle_relax(pb, c)[:, 0]
+    assert np.array_equal(got, want), cfg
+
+
+# ---------------------------------------------------------------------------
+# PhysicalStateError inside a cycle: recorded, not raised
+# ---------------------------------------------------------------------------
+
+def _sw_div():
+    path = os.path.join(GOLDEN, "sw_diverge_cases.json")
+    return {m["name"]: m for m in json.load(open(path))}
+
+
+SWDIV = _sw_div()
+
+
+@pytest.mark.parametrize("name", sorted(SWDIV))
+def test_sw_physical_state_divergence(name):
+    spec = SWDIV[name]
+    data = np.load(os.path.join(GOLDEN, "sw_diverge_cases.npz"))
+    sg = P.SpatialGrid(spec["length"], spec["n_x"])
+    tg = P.TemporalGrid(spec["horizon"], spec["n_t"])
+    model = P.make_model("shallow-water", gravity=spec["gravity"])
+    steppers = P.build_steppers(model, sg, tg, n_levels=spec["n_levels"], m=spec["m"],
+                                weno_order=spec["weno_order"], stepper=spec["stepper"],
+                                flux=spec["flux"])
+    u0 = P.harness.named_ic(spec["ic"], sg)
+    assert np.array_equal(u0, data[name + "__u0"])
+    opts = P.MgritOptions(n_levels=spec["n_levels"], m=spec["m"], cycle=spec["cycle"],
+                          relaxation=spec["relaxation"], guess=spec["guess"],
+                          max_iters=spec["max_iters"])
+    ref = None
+    if spec["has_reference"]:
+        ref = P.solve_serial(steppers[0], u0, tg, sg, model).device_values
+    if spec["outcome"] == "raises":
+        with pytest.raises(P.PhysicalStateError):
+            P.mgrit_solve(steppers, u0, tg, sg, opts, reference=ref)
+        return
+    _, rec = P.mgrit_solve(steppers, u0, tg, sg, opts, reference=ref)
+    assert rec.diverged_at == spec["diverged_at"], name
+    assert rec.diverged == (spec["diverged_at"] is not None)
+    for what in ("residuals", "errors"):
+        want = data[f"{name}__{what}"]
+        got = getattr(rec, what)
+        ok = np.isfinite(want)
+        assert np.array_equal(np.isfinite(got), ok), (name, what)
+        np.testing.assert_allclose(got[ok], want[ok], rtol=1e-10, atol=0, err_msg=name)
+    # the status word is clear afterwards: the config's admissible original
+    # (T = 0.5, N_t = 400) solves without raising
+    tg2 = P.TemporalGrid(0.5, 400)
+    st2 = P.build_steppers(model, sg, tg2, n_levels=spec["n_levels"], m=spec["m"],
+                           weno_order=spec["weno_order"], stepper=spec["stepper"],
+                           flux=spec["flux"])
+    _, rec2 = P.mgrit_solve(st2, u0, tg2, sg, P.MgritOptions(
+        n_levels=spec["n_levels"], m=spec["m"], relaxation=spec["relaxation"], max_iters=2))
+    assert not rec2.diverged

@@ -31,6 +31,17 @@ def test_config_errors_mirror_reference():
     with pytest.raises(P.ConfigError):           # beyond the system kernel's mesh limit
         P.SemiDiscreteOperator(P.make_model("euler"), P.SpatialGrid(1.0, 4096),
                                P.FluxConfig("roe", P.WenoConfig(3)))
+    # WENO5 Burgers above 4096 cells: only meshes that split into 2/4/8/16
+    # equal slabs of <= 4096 cells (the library returns MGP_EINVAL otherwise)
+    for bad_nx in (8193, 8202, 9003, 65535):
+        assert not P._lib.mesh_supported(bad_nx)
+        with pytest.raises(P.ConfigError):
+            P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, bad_nx),
+                                   P.FluxConfig("lf", P.WenoConfig(5)))
+    for good_nx, cs in ((8190, 2), (8192, 2), (12288, 4), (65536, 16), (40000, 16)):
+        assert P._lib.split_cluster_size(good_nx) == cs, good_nx
+        P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, good_nx),
+                               P.FluxConfig("lf", P.WenoConfig(5)))
     op = P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, 8),
                                 P.FluxConfig("lf", P.WenoConfig(3)))
     with pytest.raises(P.ConfigError):
