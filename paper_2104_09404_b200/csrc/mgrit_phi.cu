@@ -404,6 +404,32 @@ __device__ __forceinline__ double weno_value_rc(const double *beta, const double
     return v;
 }
 
+// weno_value_rc without its branch: the range test is AND-ed into `ok` and
+// the caller redoes the values exactly when it fails (reconstruct_centred).
+template <int K>
+__device__ __forceinline__ double weno_value_nc(const double *beta, const double *q, double eps,
+                                                bool &ok) {
+    constexpr unsigned kLo = 963u << 20;      // high word of 2^-60
+    constexpr unsigned kSpan = 121u << 20;    // [2^-60, 2^61)
+    double e[K + 1];
+#pragma unroll
+    for (int r = 0; r <= K; ++r) {
+        e[r] = eps + beta[r];
+        ok &= ((unsigned)__double2hiint(e[r]) - kLo) < kSpan;
+    }
+    double raw[K + 1];
+#pragma unroll
+    for (int r = 0; r <= K; ++r) raw[r] = mgp::div_nocheck(DW(K, r), shared_rcp(e[r] * e[r]));
+    double S = raw[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) S = S + raw[r];
+    const SharedRcp R = shared_rcp(S);
+    double v = mgp::div_nocheck(raw[0], R) * q[0];
+#pragma unroll
+    for (int r = 1; r <= K; ++r) v = v + mgp::div_nocheck(raw[r], R) * q[r];
+    return v;
+}
+
 struct Consts {
     double dt, hdt, qdt, tdt, two3, inv_dx, dx, eps, speed, half_alpha_adv;
     double k0_omega;
@@ -641,26 +667,96 @@ struct Field {
     // iteration, so no window is evaluated twice and nothing is carried
     // between iterations; the fully unrolled loop keeps the sliding window
     // in registers without copies.
+    __device__ __forceinline__ void store_states(int c, double ul, double ur) {
+        if (CS == 1) {
+            s_L[sk(c == ns ? 0 : c)] = ul;
+        } else if (c == ns) {
+            r_L_right[sk(0)] = ul;      // L state of the neighbour's interface 0
+            r_edge_right[1] = ur;       // R state of the slab's last interface
+        } else {
+            s_L[sk(c)] = ul;
+            if (c == ns - 1) r_edge_right[0] = ul;
+        }
+        s_R[sk(c - 1)] = ur;
+    }
+
+    // The whole run with the fast-path division sequences and NO branch: the
+    // validity tests of every state of the run are AND-ed into one flag that
+    // is examined after the loop, so the fully unrolled loop is one basic
+    // block and the scheduler can overlap one window's beta products with
+    // the previous window's division chains (and the left with the right
+    // state's).  A run with any state outside the fast-path range is redone
+    // by reconstruct_run_exact (out of line).
     __device__ __forceinline__ unsigned long long reconstruct_centred(const Consts &k) {
         unsigned long long m = 0;
         constexpr bool kCheck = (MODEL != MGP_MODEL_BURGERS);
         constexpr bool burg = (MODEL == MGP_MODEL_BURGERS);
         const int n = (ns - i0 < PC) ? ns - i0 : PC;
         if (n <= 0) return 0;
+        if (n < PC) return reconstruct_run_exact(k, n, true);
         double win[2 * K + 1];
 #pragma unroll
         for (int t = 0; t < 2 * K; ++t) win[t + 1] = cell(i0 + 1 - K + t);
+        bool ok = true;
         MGP_UNROLL(MGP_CENTRED_UNROLL)
         for (int p = 0; p < PC; ++p) {
-            if (p >= n) break;
             const int c = i0 + 1 + p;
 #pragma unroll
             for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
             win[2 * K] = cell(c + K);
-            bool bad = false;
+            double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
+#pragma unroll
+            for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl[s], br[K - s]);
+#pragma unroll
+            for (int r = 0; r <= K; ++r) {
+                ql[r] = cand_left<K, REG>(win, r);
+                qr[r] = cand_right<K, REG>(win, r);
+            }
+            double ul = weno_value_nc<K>(bl, ql, k.eps, ok);
+            double ur = weno_value_nc<K>(br, qr, k.eps, ok);
             if (kCheck) {
+                bool bad = false;
 #pragma unroll
                 for (int t = 0; t <= 2 * K; ++t) bad |= !is_finite(win[t]);
+                if (bad) {
+                    ul = __longlong_as_double(kNaNBits);
+                    ur = ul;
+                }
+            }
+            store_states(c, ul, ur);
+            if (burg) {
+                m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
+                // a non-finite cell makes the reference's alpha NaN
+                if (!is_finite(win[K])) m = kNaNBits;
+            }
+        }
+        if (!ok) m = reconstruct_run_exact(k, n, false);
+        return m;
+    }
+
+    // The run's states with IEEE division (weno.py:161-177 as written):
+    // `all` = every state of the run (a partial run); otherwise only the
+    // states the fast pass could not take exactly.  Burgers: a window with a
+    // non-finite cell means a non-finite cell in the field, hence a NaN alpha
+    // and NaN fluxes everywhere (flux.py:77-88) -- its states cannot reach the
+    // result and keep the fast values (`moot`), and the run's alpha bits are
+    // NaN.  Returns the run's alpha bits.
+    __device__ __noinline__ unsigned long long reconstruct_run_exact(const Consts &k, int n,
+                                                                     bool all) {
+        unsigned long long m = 0;
+        constexpr bool kCheck = (MODEL != MGP_MODEL_BURGERS);
+        constexpr bool burg = (MODEL == MGP_MODEL_BURGERS);
+        for (int p = 0; p < n; ++p) {
+            const int c = i0 + 1 + p;
+            double win[2 * K + 1];
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) win[t] = cell(c - K + t);
+            bool bad = false;
+#pragma unroll
+            for (int t = 0; t <= 2 * K; ++t) bad |= !is_finite(win[t]);
+            if (burg && bad && !all) {
+                m = kNaNBits;
+                continue;
             }
             double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
 #pragma unroll
@@ -670,26 +766,16 @@ struct Field {
                 ql[r] = cand_left<K, REG>(win, r);
                 qr[r] = cand_right<K, REG>(win, r);
             }
-            double ul = weno_value_rc<K>(bl, ql, k.eps, burg ? win : nullptr);
-            double ur = weno_value_rc<K>(br, qr, k.eps, burg ? win : nullptr);
+            double ul = weno_value_ieee<K>(bl, ql, k.eps);
+            double ur = weno_value_ieee<K>(br, qr, k.eps);
             if (kCheck && bad) {
                 ul = __longlong_as_double(kNaNBits);
                 ur = ul;
             }
-            if (CS == 1) {
-                s_L[sk(c == ns ? 0 : c)] = ul;
-            } else if (c == ns) {
-                r_L_right[sk(0)] = ul;      // L state of the neighbour's interface 0
-                r_edge_right[1] = ur;       // R state of the slab's last interface
-            } else {
-                s_L[sk(c)] = ul;
-                if (c == ns - 1) r_edge_right[0] = ul;
-            }
-            s_R[sk(c - 1)] = ur;
+            store_states(c, ul, ur);
             if (burg) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
-                // a non-finite cell makes the reference's alpha NaN
-                if (!is_finite(win[K])) m = kNaNBits;
+                if (!is_finite(win[K]) || bad) m = kNaNBits;
             }
         }
         return m;

@@ -117,6 +117,57 @@ class DistMgritHierarchy:
     def _regime(self, l):
         return dev.regime_for_batch(self.c[l])
 
+    def _fcf_workspace(self):
+        """Workspace of the fused FCF kernel for the local intervals (None
+        when the kernel does not cover the propagator, or under the CPU test
+        emulator: the sweeps are used then)."""
+        if not hasattr(self, "_fcf_ws"):
+            ws = None
+            n0 = self.nloc[0]
+            if n0 >= 1 and self.c[0] >= 2:
+                phi = self._phi(0, self._regime(0))
+                nb = dev.fcf_workspace_bytes(phi, max(n0, 2), self.options.m)
+                if nb > 0:
+                    ws = torch.zeros(nb, dtype=torch.uint8, device=self.device)
+            self._fcf_ws = ws
+        return self._fcf_ws
+
+    def relax_fine_values(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """``relax(0)`` with this rank's relaxed finest nodes off*m ..
+        (off+n0)*m materialised into ``out`` (n0*m + 1 rows, incl. the right
+        halo): the N = 1 fused kernel (mgp_relax_fcf, F-points stored) over
+        the local intervals, then the boundary exchange, then -- ranks > 0 --
+        the final F-steps of the first local interval from the new C-point
+        the left neighbour computed (the fused launch ran them from the old
+        one; this overwrites them, stream-ordered)."""
+        m, nx, n0 = self.options.m, self.nx, self.nloc[0]
+        ws = self._fcf_workspace() if self.options.relaxation == "fcf" else None
+        if out is None:
+            out = torch.empty(n0 * m + 1, nx, dtype=dev.DTYPE, device=self.device)
+        else:
+            out = out.view(n0 * m + 1, nx)
+        if ws is None:
+            self.relax(0)
+            out.copy_(self._local_values())
+            return out
+        self.f_relax(0)
+        src = self._cur
+        d = self._other(src)
+        regime = self._regime(0)
+        phi = self._phi(0, regime)
+        cs, cd = self._c[src], self._c[d]
+        dev.relax_fcf(phi, n_chunks=n0, m=m, g_mode=G_ZERO, cs=cs, cd=cd, workspace=ws,
+                      fstore=out[1], f_cs=m * nx, f_ss=nx, cstore=out, cst_s=m * nx,
+                      f0_start=None if self.r == 0 else cs[0], what="relax_fine_values")
+        self._send_right([cd[n0]], [cd[0]])
+        if self.r > 0:
+            out[0].copy_(cd[0])
+            dev.sweep(phi, n_chunks=1, start=cd[0], start_stride=0, n_steps=m - 1,
+                      g_mode=G_ZERO, store=out[1], st_ss=nx, what="relax_fine_values/f0")
+        self._cur = self._fsrc = d
+        self._pristine = False
+        return out
+
     def _other(self, i):
         if self._c[1 - i] is None:
             self._c[1 - i] = torch.empty_like(self._c[i])
@@ -124,22 +175,21 @@ class DistMgritHierarchy:
 
     def _send_right(self, last_rows, first_rows):
         """Every rank sends ``last_rows`` (its halo rows) to rank r+1, which
-        stores them into its ``first_rows``."""
+        receives them straight into its ``first_rows`` (rows of contiguous
+        level arrays, so no staging copies).  With NCCL, ``wait()`` orders the
+        current CUDA stream after the transfer without blocking the host
+        (the exchange is stream-ordered like the kernels around it); with
+        gloo (CPU tests) it is a host wait."""
         ops = []
         if self.r + 1 < self.R:
             for t in last_rows:
-                ops.append(dist.P2POp(dist.isend, t.contiguous(), self.r + 1, self.group))
-        bufs = []
+                ops.append(dist.P2POp(dist.isend, t, self.r + 1, self.group))
         if self.r > 0:
             for t in first_rows:
-                b = torch.empty_like(t)
-                bufs.append((t, b))
-                ops.append(dist.P2POp(dist.irecv, b, self.r - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, t, self.r - 1, self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
-        for t, b in bufs:
-            t.copy_(b)
 
     def _gather_rows(self, rows: torch.Tensor):
         """rows (k, nx) from every rank -> rank 0 gets a list in rank order."""
@@ -161,18 +211,21 @@ class DistMgritHierarchy:
             dist.scatter(out, None, src=0, group=self.group)
         return out
 
-    def _allsum(self, vals):
-        t = torch.tensor(vals, dtype=dev.DTYPE, device=self.device)
-        out = [torch.empty_like(t) for _ in range(self.R)]
-        dist.all_gather(out, t, group=self.group)
-        acc = torch.zeros_like(t)
-        for o in out:       # fixed rank order: identical on every rank
-            acc = acc + o
-        return acc.cpu().tolist()
-
-    def _local_reduce(self, n):
+    def _reduced(self, n) -> list:
+        """This rank's partial sums of ``n`` chunks (deterministic order,
+        mgp_sum_partials), all-gathered and added in rank order ON THE
+        DEVICE -- identical on every rank -- then read once."""
         dev.sum_partials(self._partials, n, 3, self._sums)
-        return self._sums[:3].cpu().tolist()
+        mine = self._sums[:3].contiguous()
+        if self.R == 1:
+            return mine.cpu().tolist()
+        parts = torch.empty(self.R * 3, dtype=dev.DTYPE, device=self.device)
+        dist.all_gather_into_tensor(parts, mine, group=self.group)
+        parts = parts.view(self.R, 3)
+        acc = parts[0]
+        for q in range(1, self.R):      # fixed rank order
+            acc = acc + parts[q]
+        return acc.cpu().tolist()
 
     # -- level operations -------------------------------------------------------
 
@@ -206,14 +259,23 @@ class DistMgritHierarchy:
                           what="c_relax")
             else:
                 src = self._fsrc
+                ws = self._fcf_workspace()
                 if self._cur == src:
                     d = self._other(src)
-                    self._c[d][0].copy_(self._c[src][0])
+                    if ws is None:
+                        self._c[d][0].copy_(self._c[src][0])
                     self._cur = d
                 dst = self._c[self._cur]
-                dev.sweep(phi, n_chunks=n0, start=self._c[src], start_stride=nx,
-                          n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI, tail_regime=regime,
-                          tail_g_mode=G_ZERO, tail_out=dst[1], to_s=nx, what="c_relax")
+                if ws is not None:
+                    # the N = 1 fused kernel over the local intervals (node 0
+                    # copied by the kernel; ranks > 0 receive it below)
+                    dev.relax_fcf(phi, n_chunks=n0, m=m, g_mode=G_ZERO, cs=self._c[src],
+                                  cd=dst, workspace=ws, what="c_relax")
+                else:
+                    dev.sweep(phi, n_chunks=n0, start=self._c[src], start_stride=nx,
+                              n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
+                              tail_regime=regime, tail_g_mode=G_ZERO, tail_out=dst[1],
+                              to_s=nx, what="c_relax")
             self._send_right([dst[n0]], [dst[0]])
             self._pristine = False
             return
@@ -387,12 +449,13 @@ class DistMgritHierarchy:
             dev.sweep(self._phi(0, resid_regime), n_chunks=1, start=self._u0, start_stride=0,
                       tail=TAIL_RESID, tail_regime=resid_regime, tail_g_mode=G_ZERO,
                       aux=self._u0, aux_s=0, partials=self._partials, what="residual")
-            r2 = self._local_reduce(1)[0]
+            dev.sum_partials(self._partials, 1, 3, self._sums)
+            r2 = float(self._sums[0].item())
             rows = n0 * m + last
             dev.sweep(self._phi(0, resid_regime), n_chunks=rows, start=self._u0,
                       start_stride=0, ref=ref, ref_cs=nx, count_nonfinite=1,
                       partials=self._partials, what="monitor")
-            _, e2, nf = self._allsum(self._local_reduce(rows))
+            _, e2, nf = self._reduced(rows)
             return Monitor(math.sqrt(nt * r2), e2, int(nf))
         if self._fsrc == self._cur and self._regime(0) == SUM_SEQ:
             c = self._c[self._cur]
@@ -401,14 +464,14 @@ class DistMgritHierarchy:
                       ref_last_next=last, count_nonfinite=1, tail=TAIL_RESID,
                       tail_regime=resid_regime, tail_g_mode=G_ZERO, aux=c[1], aux_s=nx,
                       partials=self._partials, what="monitor")
-            r2, e2, nf = self._allsum(self._local_reduce(n0))
+            r2, e2, nf = self._reduced(n0)
             return Monitor(math.sqrt(r2), e2, int(nf))
         traj = self._local_values().reshape(-1, nx)       # n0*m + 1 rows
         dev.sweep(self._phi(0, resid_regime), n_chunks=n0 * m, start=traj, start_stride=nx,
                   ref=ref, ref_cs=nx, count_nonfinite=1, tail=TAIL_RESID,
                   tail_regime=resid_regime, tail_g_mode=G_ZERO, aux=traj[1], aux_s=nx,
                   ref_last_next=last, partials=self._partials, what="monitor")
-        r2, e2, nf = self._allsum(self._local_reduce(n0 * m))
+        r2, e2, nf = self._reduced(n0 * m)
         return Monitor(math.sqrt(r2), e2, int(nf))
 
     def residual_norm(self) -> float:
@@ -499,6 +562,8 @@ def mgrit_solve_distributed(steppers, initial_state, time_grid, space_grid,
         n = len(dev.STATUS_BITS)
         return dev.bits_to_status(f[:n]), dev.bits_to_status(f[n:])
 
+    if checked:
+        dev.take_status()      # stale bits of earlier, unrelated work
     mon = h.monitor(ref)
     if checked:
         dev.raise_for_status(status_bits(None)[1])
@@ -524,4 +589,6 @@ def mgrit_solve_distributed(steppers, initial_state, time_grid, space_grid,
         errors[it], residuals[it] = err, mon.residual
     v = h.fine_values()
     traj = Trajectory(time_grid, space_grid, v.cpu().numpy()) if v is not None else None
+    if checked:
+        dev.take_status()      # F-point recomputation of a diverged iterate (see mgrit.py)
     return traj, ConvergenceRecord(errors, residuals, diverged, at)

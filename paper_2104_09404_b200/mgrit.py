@@ -690,10 +690,21 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     if hierarchy_out is not None:
         hierarchy_out.append(h)
 
+    checked = h.n_components > 1    # systems: PhysicalStateError
+
     def trajectory():
         if not return_trajectory:
             return None
-        return Trajectory(time_grid, space_grid, h.fine_values().cpu().numpy())
+        t = Trajectory(time_grid, space_grid, h.fine_values().cpu().numpy())
+        if checked:
+            # the reference's fine_values() returns stored arrays and never
+            # raises; bits set recomputing a diverged iterate's F-points here
+            # belong to no propagator call of the solve
+            dev.take_status()
+        return t
+
+    if checked:
+        dev.take_status()      # stale bits of earlier, unrelated work
 
     if options.max_iters == 0:
         return trajectory(), ConvergenceRecord(errors=np.empty(0), residuals=np.empty(0))
@@ -717,7 +728,6 @@ def mgrit_solve(steppers: Sequence, initial_state, time_grid: TemporalGrid,
     errors = np.full(n_rows, np.nan)
     residuals = np.full(n_rows, np.nan)
     diverged, diverged_at, converged_at = False, None, None
-    checked = h.n_components > 1    # shallow water: PhysicalStateError
 
     def watch(mon):
         if checked:
