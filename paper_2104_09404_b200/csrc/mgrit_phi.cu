@@ -196,11 +196,24 @@ constexpr int kModelBurgersRoe = 8;
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
 #define MGP_UNROLL(n) MGP_UNROLL_(n)
 
-// Shared-memory index of element t: one pad word per 16 elements, so that
-// the lanes of a warp walking runs of P in {1,2,4,8} consecutive cells hit
-// distinct banks.
-__device__ __forceinline__ int sk(int t) { return t + (t >> 4); }
-__host__ __device__ constexpr int sk_size(int n) { return n + (n >> 4) + 1; }
+// Shared-memory index of element t: one pad word per 2^LG elements, so that
+// the lanes of a warp walking runs of P consecutive cells hit distinct banks.
+// LG = log2(P) for runs of 4 or 8 cells (a thread's first cell i0 is then a
+// multiple of 2^LG, so sk(i0 + x) = sk(i0) + x + (x >> LG) for any x: every
+// address of the unrolled hot loops is the thread's base plus a literal),
+// one pad per 16 elements otherwise.  A half-warp's 64-bit accesses at
+// thread stride 2^LG + 1 words fall into 16 distinct bank pairs.
+__host__ __device__ constexpr int pad_log(int p) { return p == 8 ? 3 : (p == 4 ? 2 : 4); }
+template <int LG>
+__host__ __device__ constexpr int skp(int t) { return t + (t >> LG); }
+template <int LG>
+__host__ __device__ constexpr int skp_size(int n) { return n + (n >> LG) + 1; }
+
+// The dynamic shared memory of every kernel of the WENO/RK Field family, as
+// one array: Field addresses it by element offsets, so every access is a
+// shared-space LDS/STS with a 32-bit address (pointers kept in the Field
+// struct decayed to generic 64-bit loads and stores).
+extern __shared__ double mgp_sm[];
 
 // ---------------------------------------------------------------------------
 // WENO reconstruction, reference weno.py:154-177, for a run of consecutive
@@ -470,25 +483,61 @@ struct Field {
     // (warps alternate between left and right states), one cell per thread
     // in the cell phases.  Otherwise P cells/interfaces per thread.
     static constexpr int PC = P == 0 ? 1 : P;
+    static constexpr int LG = pad_log(P);
+    static __host__ __device__ constexpr int sk(int t) { return skp<LG>(t); }
+    static __host__ __device__ constexpr int sk_size(int n) { return skp_size<LG>(n); }
     int ns, run, i0, q;
-    double *s_u;   // stage input, local cell t at s_u[sk(t + H)], t in [-H, ns + H)
-    double *s_L;   // left states, then interface fluxes, at s_L[sk(i)]
-    double *s_R;   // right states, then results, at s_R[sk(i)]
-    double *s_u0;  // RK base state of the cells, at s_u0[sk(t)]
-    unsigned long long *s_red;
-    double *s_edge;                // [2] states of the interface left of the slab
-    unsigned long long *s_cmax;    // [CS] per-CTA alpha bits
+    // element offsets into mgp_sm (shared-space addressing):
+    int o_u;    // stage input, local cell t at o_u + sk(t + H), t in [-H, ns + H)
+    int o_L;    // left states, then interface fluxes, at o_L + sk(i)
+    int o_R;    // right states, then results, at o_R + sk(i)
+    int o_u0;   // RK base state of the cells, at o_u0 + sk(t)
+    int o_red;  // [32] per-warp alpha bits
+    int o_edge;                    // [2] states of the interface left of the slab
+    int o_cmax;                    // [CS] per-CTA alpha bits
+    int b;                         // sk(i0): the thread's base (i0 a multiple of 2^LG)
     double *r_u_left, *r_u_right;  // neighbours' s_u (distributed shared memory)
     double *r_edge_right;          // right neighbour's s_edge
     double *r_L_right;             // right neighbour's s_L (centred reconstruction)
+    // lay the arrays out from element offset `at`; returns the end offset
+    __device__ __forceinline__ int layout(int at, int ns_, int tid) {
+        ns = ns_;
+        run = tid;
+        i0 = tid * PC;
+        b = sk(i0);
+        o_u = at;
+        o_L = o_u + sk_size(ns + 2 * H);
+        o_R = o_L + sk_size(ns);
+        o_u0 = o_R + sk_size(ns);
+        return o_u0 + sk_size(ns);
+    }
+    __device__ __forceinline__ double &s_u(int idx) const { return mgp_sm[o_u + idx]; }
+    __device__ __forceinline__ double &s_L(int idx) const { return mgp_sm[o_L + idx]; }
+    __device__ __forceinline__ double &s_R(int idx) const { return mgp_sm[o_R + idx]; }
+    __device__ __forceinline__ double &s_u0(int idx) const { return mgp_sm[o_u0 + idx]; }
+    __device__ __forceinline__ unsigned long long &s_red(int w) const {
+        return reinterpret_cast<unsigned long long *>(mgp_sm)[o_red + w];
+    }
+    __device__ __forceinline__ double &s_edge(int j) const { return mgp_sm[o_edge + j]; }
+    __device__ __forceinline__ unsigned long long &s_cmax(int j) const {
+        return reinterpret_cast<unsigned long long *>(mgp_sm)[o_cmax + j];
+    }
+    // thread-relative accessors (runs of 4 or 8 cells): element i0 + x with
+    // x a literal after unrolling -> base register + immediate
+    static constexpr bool kRel = (P == 4 || P == 8);
+    static __host__ __device__ constexpr int rel(int x) { return x + (x >> LG); }
+    __device__ __forceinline__ double &u_rel(int x) const { return mgp_sm[o_u + b + rel(x + H)]; }
+    __device__ __forceinline__ double &L_rel(int x) const { return mgp_sm[o_L + b + rel(x)]; }
+    __device__ __forceinline__ double &R_rel(int x) const { return mgp_sm[o_R + b + rel(x)]; }
+    __device__ __forceinline__ double &u0_rel(int x) const { return mgp_sm[o_u0 + b + rel(x)]; }
     // barrier over the CTAs sharing the field (hardware cluster barrier; an
     // mbarrier-based all-to-all with one arriving thread per CTA measured
     // 1.8-2.5x slower per stage on B200)
     __device__ __forceinline__ void sync() { field_sync<CS>(); }
 
     static constexpr int HALO = H;
-    __device__ __forceinline__ double cell(int t) const { return s_u[sk(t + H)]; }
-    __device__ __forceinline__ void load(int t, double v) { s_u[sk(t + H)] = v; }
+    __device__ __forceinline__ double cell(int t) const { return s_u(sk(t + H)); }
+    __device__ __forceinline__ void load(int t, double v) { s_u(sk(t + H)) = v; }
     // centred reconstruction with the merged flux / rhs pass: the interface
     // states stay readable by neighbouring runs until the stage ends, so
     // results go to the RK base slots, which only their owner reads.  On a
@@ -503,13 +552,13 @@ struct Field {
         P > 0 && K > 0;
 #endif
     __device__ __forceinline__ double result(int t) const {
-        return kMerged ? s_u0[sk(t)] : s_R[sk(t)];
+        return kMerged ? s_u0(sk(t)) : s_R(sk(t));
     }
     __device__ __forceinline__ void put(int t, double v) {
-        s_u[sk(t + H)] = v;
+        s_u(sk(t + H)) = v;
         if (CS == 1) {
-            if (t < H) s_u[sk(ns + H + t)] = v;
-            if (t >= ns - H) s_u[sk(t - (ns - H))] = v;
+            if (t < H) s_u(sk(ns + H + t)) = v;
+            if (t >= ns - H) s_u(sk(t - (ns - H))) = v;
         } else {
             if (t < H) r_u_left[sk(ns + H + t)] = v;
             if (t >= ns - H) r_u_right[sk(t - ns + H)] = v;
@@ -553,8 +602,8 @@ struct Field {
             }
             double v = weno_value<K>(b, q, k.eps, nullptr, MODEL == MGP_MODEL_BURGERS && badw);
             if (kCheck && badw) v = __longlong_as_double(kNaNBits);
-            if (side == 0) s_L[sk(i)] = v;
-            else s_R[sk(i)] = v;
+            if (side == 0) s_L(sk(i)) = v;
+            else s_R(sk(i)) = v;
             if (CS > 1 && i == ns - 1) r_edge_right[side] = v;
             if (MODEL == MGP_MODEL_BURGERS) {
                 m = abs_bits(v);
@@ -578,8 +627,8 @@ struct Field {
                     if (!is_finite(c0)) ul = __longlong_as_double(kNaNBits);
                     if (!is_finite(c1)) ur = __longlong_as_double(kNaNBits);
                 }
-                s_L[sk(i)] = ul;
-                s_R[sk(i)] = ur;
+                s_L(sk(i)) = ul;
+                s_R(sk(i)) = ur;
                 if (CS > 1 && i == ns - 1) {
                     r_edge_right[0] = ul;
                     r_edge_right[1] = ur;
@@ -639,8 +688,8 @@ struct Field {
                 if (bad_left) ul = __longlong_as_double(kNaNBits);
                 if (bad_right) ur = __longlong_as_double(kNaNBits);
             }
-            s_L[sk(i)] = ul;
-            s_R[sk(i)] = ur;
+            s_L(sk(i)) = ul;
+            s_R(sk(i)) = ur;
             if (CS > 1 && i == ns - 1) {
                 r_edge_right[0] = ul;
                 r_edge_right[1] = ur;
@@ -669,15 +718,32 @@ struct Field {
     // in registers without copies.
     __device__ __forceinline__ void store_states(int c, double ul, double ur) {
         if (CS == 1) {
-            s_L[sk(c == ns ? 0 : c)] = ul;
+            s_L(sk(c == ns ? 0 : c)) = ul;
         } else if (c == ns) {
             r_L_right[sk(0)] = ul;      // L state of the neighbour's interface 0
             r_edge_right[1] = ur;       // R state of the slab's last interface
         } else {
-            s_L[sk(c)] = ul;
+            s_L(sk(c)) = ul;
             if (c == ns - 1) r_edge_right[0] = ul;
         }
-        s_R[sk(c - 1)] = ur;
+        s_R(sk(c - 1)) = ur;
+    }
+    // the same for window p of a full run (c = i0 + 1 + p <= ns, equality
+    // only for the last window of the field's last run): literal offsets
+    __device__ __forceinline__ void store_states_rel(int p, double ul, double ur) {
+        const int c = i0 + 1 + p;
+        if (p == PC - 1 && c == ns) {
+            if (CS == 1) {
+                s_L(0) = ul;
+            } else {
+                r_L_right[0] = ul;
+                r_edge_right[1] = ur;
+            }
+        } else {
+            L_rel(1 + p) = ul;
+            if (CS > 1 && p >= PC - 2 && c == ns - 1) r_edge_right[0] = ul;
+        }
+        R_rel(p) = ur;
     }
 
     // The whole run with the fast-path division sequences and NO branch: the
@@ -696,14 +762,15 @@ struct Field {
         if (n < PC) return reconstruct_run_exact(k, n, true);
         double win[2 * K + 1];
 #pragma unroll
-        for (int t = 0; t < 2 * K; ++t) win[t + 1] = cell(i0 + 1 - K + t);
+        for (int t = 0; t < 2 * K; ++t)
+            win[t + 1] = kRel ? u_rel(1 - K + t) : cell(i0 + 1 - K + t);
         bool ok = true;
         MGP_UNROLL(MGP_CENTRED_UNROLL)
         for (int p = 0; p < PC; ++p) {
             const int c = i0 + 1 + p;
 #pragma unroll
             for (int t = 0; t < 2 * K; ++t) win[t] = win[t + 1];
-            win[2 * K] = cell(c + K);
+            win[2 * K] = kRel ? u_rel(1 + p + K) : cell(c + K);
             double bl[K + 1], br[K + 1], ql[K + 1], qr[K + 1];
 #pragma unroll
             for (int s = 0; s <= K; ++s) beta_block<K, true>(win, s, bl[s], br[K - s]);
@@ -723,7 +790,8 @@ struct Field {
                     ur = ul;
                 }
             }
-            store_states(c, ul, ur);
+            if (kRel) store_states_rel(p, ul, ur);
+            else store_states(c, ul, ur);
             if (burg) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
                 // a non-finite cell makes the reference's alpha NaN
@@ -822,21 +890,21 @@ struct Field {
         if (MODEL == MGP_MODEL_BURGERS) {
             m = warp_umax64(m);
             const int tid = threadIdx.x;
-            if ((tid & 31) == 0) s_red[tid >> 5] = m;
+            if ((tid & 31) == 0) s_red(tid >> 5) = m;
             __syncthreads();
-            m = s_red[0];
+            m = s_red(0);
             const int nw = (blockDim.x + 31) >> 5;
-            for (int w = 1; w < nw; ++w) m = umax64(m, s_red[w]);
+            for (int w = 1; w < nw; ++w) m = umax64(m, s_red(w));
             if (CS > 1) {
                 if (threadIdx.x == 0) {
                     cg::cluster_group cl = cg::this_cluster();
 #pragma unroll
-                    for (int j = 0; j < CS; ++j) cl.map_shared_rank(s_cmax, j)[q] = m;
+                    for (int j = 0; j < CS; ++j) cl.map_shared_rank(&s_cmax(0), j)[q] = m;
                 }
                 sync();   // also publishes the pushed edge states
-                m = s_cmax[0];
+                m = s_cmax(0);
 #pragma unroll
-                for (int j = 1; j < CS; ++j) m = umax64(m, s_cmax[j]);
+                for (int j = 1; j < CS; ++j) m = umax64(m, s_cmax(j));
             }
             half_alpha = 0.5 * __longlong_as_double((long long)m);
         } else {
@@ -852,15 +920,18 @@ struct Field {
             // itself (one extra flux per run) instead of a flux pass, a
             // barrier and a re-read
             if (i0 < ns) {
-                const int il = (i0 == 0) ? ns - 1 : i0 - 1;
+                // interface left of the run: sk(i0 - 1) = b + rel(-1)
+                const int il = (i0 == 0) ? sk(ns - 1) : (kRel ? b + rel(-1) : sk(i0 - 1));
                 double fm = (CS > 1 && i0 == 0)
-                                ? lf(k, s_edge[0], s_edge[1], half_alpha)
-                                : lf(k, s_L[sk(il)], s_R[sk(il)], half_alpha);
+                                ? lf(k, s_edge(0), s_edge(1), half_alpha)
+                                : lf(k, s_L(il), s_R(il), half_alpha);
+                const bool full = kRel && i0 + PC <= ns;
 #pragma unroll
                 for (int p = 0; p < PC; ++p) {
                     const int c = i0 + p;
-                    if (c < ns) {
-                        const double f = lf(k, s_L[sk(c)], s_R[sk(c)], half_alpha);
+                    if (full || c < ns) {
+                        const double f = kRel ? lf(k, L_rel(p), R_rel(p), half_alpha)
+                                              : lf(k, s_L(sk(c)), s_R(sk(c)), half_alpha);
                         const double neg = -(f - fm);
                         A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
                         fm = f;
@@ -873,7 +944,7 @@ struct Field {
 #pragma unroll
         for (int p = 0; p < PC; ++p) {
             const int i = i0 + p;
-            if (i < ns) s_L[sk(i)] = lf(k, s_L[sk(i)], s_R[sk(i)], half_alpha);
+            if (i < ns) s_L(sk(i)) = lf(k, s_L(sk(i)), s_R(sk(i)), half_alpha);
         }
         __syncthreads();
 #pragma unroll
@@ -881,10 +952,10 @@ struct Field {
             const int c = i0 + p;
             if (c < ns) {
                 double fm;
-                if (c > 0) fm = s_L[sk(c - 1)];
-                else if (CS == 1) fm = s_L[sk(ns - 1)];
-                else fm = lf(k, s_edge[0], s_edge[1], half_alpha);
-                const double neg = -(s_L[sk(c)] - fm);
+                if (c > 0) fm = s_L(sk(c - 1));
+                else if (CS == 1) fm = s_L(sk(ns - 1));
+                else fm = lf(k, s_edge(0), s_edge(1), half_alpha);
+                const double neg = -(s_L(sk(c)) - fm);
                 A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
             }
         }
@@ -897,13 +968,16 @@ struct Field {
     // The RK base and the stage values live in shared memory (s_u0, s_u), so
     // no per-cell state is held in registers across the reconstruction.
     __device__ __forceinline__ double u0(int p) const {
-        return (i0 + p < ns) ? s_u0[sk(i0 + p)] : 0.0;
+        return (i0 + p < ns) ? (kRel ? u0_rel(p) : s_u0(sk(i0 + p))) : 0.0;
     }
 
     __device__ __forceinline__ void phi(const Consts &k, int rk) {
 #pragma unroll
         for (int p = 0; p < PC; ++p)
-            if (i0 + p < ns) s_u0[sk(i0 + p)] = cell(i0 + p);
+            if (i0 + p < ns) {
+                if (kRel) u0_rel(p) = u_rel(p);
+                else s_u0(sk(i0 + p)) = cell(i0 + p);
+            }
         const int stages = rk == 0 ? 1 : rk;
         // one call site of the reconstruction for every stage (code size)
 #pragma unroll 1
@@ -936,10 +1010,32 @@ struct Field {
     }
 
     __device__ __forceinline__ double stage(int p) const {
-        return (i0 + p < ns) ? cell(i0 + p) : 0.0;
+        return (i0 + p < ns) ? (kRel ? u_rel(p) : cell(i0 + p)) : 0.0;
     }
 
     __device__ __forceinline__ void commit(const double *v) {
+        if (kRel && ns >= 2 * PC && (i0 + PC + H <= ns || i0 + PC == ns)) {
+            // full run: literal offsets; the periodic halo copies (cells
+            // [0, H) and [ns - H, ns), H <= PC) belong to the first and the
+            // last run
+#pragma unroll
+            for (int p = 0; p < PC; ++p) u_rel(p) = v[p];
+            if (i0 == 0) {
+#pragma unroll
+                for (int p = 0; p < H; ++p) {
+                    if (CS == 1) s_u(sk(ns + H + p)) = v[p];
+                    else r_u_left[sk(ns + H + p)] = v[p];
+                }
+            }
+            if (i0 + PC == ns) {
+#pragma unroll
+                for (int p = PC - H; p < PC; ++p) {
+                    if (CS == 1) s_u(sk(p - (PC - H))) = v[p];
+                    else r_u_right[sk(p - (PC - H))] = v[p];
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) put(i0 + p, v[p]);
@@ -947,7 +1043,10 @@ struct Field {
     __device__ __forceinline__ void store_res(const double *v) {
 #pragma unroll
         for (int p = 0; p < PC; ++p)
-            if (i0 + p < ns) (kMerged ? s_u0 : s_R)[sk(i0 + p)] = v[p];
+            if (i0 + p < ns) {
+                if (kRel) (kMerged ? u0_rel(p) : R_rel(p)) = v[p];
+                else (kMerged ? s_u0(sk(i0 + p)) : s_R(sk(i0 + p))) = v[p];
+            }
     }
 };
 
@@ -1103,7 +1202,6 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
 
 template <int K, int REG, int MODEL, int P, int REGS, int CS>
 __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
-    extern __shared__ double smem[];
     using F = Field<K, REG, MODEL, P, CS>;
     F f;
     const int nx = (int)a.phi.nx;
@@ -1111,25 +1209,19 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
     const int c0 = q * ns;             // global index of local cell 0
     const int tid = threadIdx.x;
-    f.ns = ns;
     f.q = q;
-    f.run = tid;
-    f.i0 = tid * F::PC;
-    f.s_u = smem;
-    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
-    f.s_R = f.s_L + sk_size(ns);
-    f.s_u0 = f.s_R + sk_size(ns);
-    double *s_sum = f.s_u0 + sk_size(ns);      // [3 * 32]
+    const int o_sum = f.layout(0, ns, tid);    // the four field arrays (smem_bytes)
+    double *s_sum = mgp_sm + o_sum;            // [3 * 32]
     double *s_psum = s_sum + 3 * 32;           // [3 * CS] cluster partials
-    f.s_edge = s_psum + 3 * CS;                // [2]
-    f.s_cmax = reinterpret_cast<unsigned long long *>(f.s_edge + 2);   // [CS]
-    f.s_red = f.s_cmax + CS;                   // [32]
+    f.o_edge = o_sum + 3 * 32 + 3 * CS;        // [2]
+    f.o_cmax = f.o_edge + 2;                   // [CS]
+    f.o_red = f.o_cmax + CS;                   // [32]
     if (CS > 1) {
         cg::cluster_group cl = cg::this_cluster();
-        f.r_u_left = cl.map_shared_rank(f.s_u, (q + CS - 1) % CS);
-        f.r_u_right = cl.map_shared_rank(f.s_u, (q + 1) % CS);
-        f.r_edge_right = cl.map_shared_rank(f.s_edge, (q + 1) % CS);
-        f.r_L_right = cl.map_shared_rank(f.s_L, (q + 1) % CS);
+        f.r_u_left = cl.map_shared_rank(&f.s_u(0), (q + CS - 1) % CS);
+        f.r_u_right = cl.map_shared_rank(&f.s_u(0), (q + 1) % CS);
+        f.r_edge_right = cl.map_shared_rank(&f.s_edge(0), (q + 1) % CS);
+        f.r_L_right = cl.map_shared_rank(&f.s_L(0), (q + 1) % CS);
     }
     sweep_body<F, CS>(a, k, f, ns, q, c0, s_sum, s_psum, nx);
 }
@@ -1450,21 +1542,14 @@ __device__ __forceinline__ void fcf_load(F &f, const double *x0, int ns, bool co
 template <int K, int REG, int MODEL, int P, int REGS>
 __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts k,
                                              const FcfPlan pl) {
-    extern __shared__ double smem[];
     __shared__ long long s_ticket, s_chain;
     using F = Field<K, REG, MODEL, P, 1>;
     F f;
     const int ns = (int)a.phi.nx;
     const int tid = threadIdx.x, nt = blockDim.x;
-    f.ns = ns;
     f.q = 0;
-    f.run = tid;
-    f.i0 = tid * F::PC;
-    f.s_u = smem;
-    f.s_L = f.s_u + sk_size(ns + 2 * F::H);
-    f.s_R = f.s_L + sk_size(ns);
-    f.s_u0 = f.s_R + sk_size(ns);
-    f.s_red = reinterpret_cast<unsigned long long *>(f.s_u0 + sk_size(ns));
+    f.o_red = f.layout(0, ns, tid);
+    f.o_edge = f.o_cmax = f.o_red;   // unused without a cluster
     // workspace (layout fixed per device and mesh, whatever the call's
     // interval count): ticket, exit and queue counters, one spare | Gmax
     // tags (segment mode) or queue slots (split plan) | Gmax rows
@@ -2215,9 +2300,12 @@ int threads_for(int64_t ns, int p) {
     return (int)nt;
 }
 
-size_t smem_bytes(int64_t ns, int k, int cs) {
+size_t smem_bytes(int64_t ns, int k, int cs, int p) {
     const int H = k + 1;
-    return sizeof(double) * (size_t)(sk_size((int)ns + 2 * H) + 3 * sk_size((int)ns) + 3 * 32 +
+    const auto size = [p](int n) {   // Field::sk_size for run length p
+        return p == 8 ? skp_size<3>(n) : (p == 4 ? skp_size<2>(n) : skp_size<4>(n));
+    };
+    return sizeof(double) * (size_t)(size((int)ns + 2 * H) + 3 * size((int)ns) + 3 * 32 +
                                      3 * cs + 2) +
            sizeof(unsigned long long) * (size_t)(cs + 32);
 }
@@ -2226,7 +2314,7 @@ template <int K, int REG, int MODEL, int P, int REGS, int CS>
 int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     const int64_t ns = a.phi.nx / CS;
     const int nt = threads_for(ns, P);
-    const size_t sm = smem_bytes(ns, K, CS);
+    const size_t sm = smem_bytes(ns, K, CS, P);
     auto kern = sweep_kernel<K, REG, MODEL, P, REGS, CS>;
     static unsigned long long attr_devs = 0;
     if (!ensure_attrs(kern, attr_devs, CS > 8)) return MGP_ECUDA;
@@ -2498,7 +2586,7 @@ int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
     auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>;
     const int ns = (int)phi.nx;
     L.nt = threads_for(ns, P);
-    L.smem = smem_bytes(ns, K, 1);
+    L.smem = smem_bytes(ns, K, 1, P);
     static unsigned long long attr_devs = 0;
     if (!ensure_attrs(kern, attr_devs, false)) return MGP_ECUDA;
     int dev = 0, nsm = 0, per = 0;

@@ -24,7 +24,7 @@ check)
     echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
     timeout 900 python bench.py --steps 10 --warmup 3 --cpu-seconds 5 > gpurun_out/bench.log 2>&1
     echo "bench rc=$?" >> gpurun_out/bench.log
-    tail -3 gpurun_out/smoke.log gpurun_out/pytest_gpu.log gpurun_out/bench.log ;;
+    tail -n 3 gpurun_out/smoke.log gpurun_out/pytest_gpu.log gpurun_out/bench.log ;;
 round)
     timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
     echo "smoke rc=$?" >> gpurun_out/smoke.log
@@ -42,13 +42,13 @@ round)
     echo "ncu rc=$?" >> gpurun_out/ncu_full.log ;;
 bench)
     timeout 900 python bench.py "$@" > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-    tail -2 gpurun_out/bench.log ;;
+    tail -n 2 gpurun_out/bench.log ;;
 ncu)
     tag=$1; regex=$2; skip=$3; shift 3
     "$@" > gpurun_out/plain_$tag.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k "regex:$regex" -s "$skip" -c 1 \
         -o gpurun_out/prof_$tag "$@" > gpurun_out/ncu_$tag.log 2>&1
-    echo "ncu rc=$?" >> gpurun_out/ncu_$tag.log; tail -3 gpurun_out/ncu_$tag.log ;;
+    echo "ncu rc=$?" >> gpurun_out/ncu_$tag.log; tail -n 3 gpurun_out/ncu_$tag.log ;;
 launches)
     tag=$1; shift
     "$@" > gpurun_out/plain_$tag.log 2>&1 && \
@@ -59,7 +59,7 @@ py)
     script=$1; shift
     base=$(basename "$script" .py)
     timeout 1800 python "$script" "$@" > gpurun_out/$base.out 2> gpurun_out/$base.err
-    echo "rc=$?" >> gpurun_out/$base.err; tail -5 gpurun_out/$base.out gpurun_out/$base.err ;;
+    echo "rc=$?" >> gpurun_out/$base.err; tail -n 5 gpurun_out/$base.out gpurun_out/$base.err ;;
 *)
     echo "unknown mode $what"; exit 2 ;;
 esac
