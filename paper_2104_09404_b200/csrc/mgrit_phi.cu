@@ -189,8 +189,16 @@ constexpr int kModelBurgersRoe = 8;
 #ifndef MGP_SLIDE_UNROLL
 #define MGP_SLIDE_UNROLL 1
 #endif
-#ifndef MGP_CENTRED_UNROLL
-#define MGP_CENTRED_UNROLL 8
+// Unroll factor of the centred reconstruction: half a run per block (two
+// blocks of 4 windows for runs of 8 cells, of 2 for runs of 4).  Measured on
+// B200 (profiles/r02_fcf_unroll.txt): C3 16.3 -> 17.8 G point-updates/s --
+// the 8-window block spilled 824 bytes at 128 registers, the 4-window block
+// none inside the loop, and its static schedule has 19 % fewer stall cycles
+// per window; C2 (runs of 4) 14.2 -> 14.6 G.  MGP_CENTRED_UNROLL overrides.
+#ifdef MGP_CENTRED_UNROLL
+#define MGP_CU(pc) MGP_CENTRED_UNROLL
+#else
+#define MGP_CU(pc) ((pc) >= 4 ? (pc) / 2 : (pc))
 #endif
 #define MGP_PRAGMA(x) _Pragma(#x)
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
@@ -203,7 +211,7 @@ constexpr int kModelBurgersRoe = 8;
 // address of the unrolled hot loops is the thread's base plus a literal),
 // one pad per 16 elements otherwise.  A half-warp's 64-bit accesses at
 // thread stride 2^LG + 1 words fall into 16 distinct bank pairs.
-__host__ __device__ constexpr int pad_log(int p) { return p == 8 ? 3 : (p == 4 ? 2 : 4); }
+__host__ __device__ constexpr int pad_log(int p) { return p == 8 ? 3 : (p == 4 ? 2 : 4); }   // 16 -> 4
 template <int LG>
 __host__ __device__ constexpr int skp(int t) { return t + (t >> LG); }
 template <int LG>
@@ -524,7 +532,8 @@ struct Field {
     }
     // thread-relative accessors (runs of 4 or 8 cells): element i0 + x with
     // x a literal after unrolling -> base register + immediate
-    static constexpr bool kRel = (P == 4 || P == 8);
+    static constexpr bool kRel = (P == 4 || P == 8 || P == 16);
+    static constexpr bool kFusedCommit = true;   // phi_commit available (sweep_body)
     static __host__ __device__ constexpr int rel(int x) { return x + (x >> LG); }
     __device__ __forceinline__ double &u_rel(int x) const { return mgp_sm[o_u + b + rel(x + H)]; }
     __device__ __forceinline__ double &L_rel(int x) const { return mgp_sm[o_L + b + rel(x)]; }
@@ -765,7 +774,8 @@ struct Field {
         for (int t = 0; t < 2 * K; ++t)
             win[t + 1] = kRel ? u_rel(1 - K + t) : cell(i0 + 1 - K + t);
         bool ok = true;
-        MGP_UNROLL(MGP_CENTRED_UNROLL)
+        constexpr int kCU = MGP_CU(PC);
+#pragma unroll(kCU)
         for (int p = 0; p < PC; ++p) {
             const int c = i0 + 1 + p;
 #pragma unroll
@@ -892,9 +902,9 @@ struct Field {
             const int tid = threadIdx.x;
             if ((tid & 31) == 0) s_red(tid >> 5) = m;
             __syncthreads();
-            m = s_red(0);
+            // at most kMaxThreads / 32 = 16 warps: one slot per lane
             const int nw = (blockDim.x + 31) >> 5;
-            for (int w = 1; w < nw; ++w) m = umax64(m, s_red(w));
+            m = warp_umax64((tid & 31) < nw ? s_red(tid & 31) : 0ull);
             if (CS > 1) {
                 if (threadIdx.x == 0) {
                     cg::cluster_group cl = cg::this_cluster();
@@ -925,16 +935,33 @@ struct Field {
                 double fm = (CS > 1 && i0 == 0)
                                 ? lf(k, s_edge(0), s_edge(1), half_alpha)
                                 : lf(k, s_L(il), s_R(il), half_alpha);
-                const bool full = kRel && i0 + PC <= ns;
+                if (kRel && i0 + PC <= ns) {
+                    // full run: straight-line code, literal offsets
+                    double neg[PC];
 #pragma unroll
-                for (int p = 0; p < PC; ++p) {
-                    const int c = i0 + p;
-                    if (full || c < ns) {
-                        const double f = kRel ? lf(k, L_rel(p), R_rel(p), half_alpha)
-                                              : lf(k, s_L(sk(c)), s_R(sk(c)), half_alpha);
-                        const double neg = -(f - fm);
-                        A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+                    for (int p = 0; p < PC; ++p) {
+                        const double f = lf(k, L_rel(p), R_rel(p), half_alpha);
+                        neg[p] = -(f - fm);
                         fm = f;
+                    }
+                    if (k.dx_pow2) {
+#pragma unroll
+                        for (int p = 0; p < PC; ++p) A[p] = neg[p] * k.inv_dx;
+                    } else {
+#pragma unroll
+                        for (int p = 0; p < PC; ++p) A[p] = neg[p] / k.dx;
+                    }
+                } else {
+#pragma unroll
+                    for (int p = 0; p < PC; ++p) {
+                        const int c = i0 + p;
+                        if (c < ns) {
+                            const double f = kRel ? lf(k, L_rel(p), R_rel(p), half_alpha)
+                                                  : lf(k, s_L(sk(c)), s_R(sk(c)), half_alpha);
+                            const double neg = -(f - fm);
+                            A[p] = k.dx_pow2 ? neg * k.inv_dx : neg / k.dx;
+                            fm = f;
+                        }
                     }
                 }
             }
@@ -971,7 +998,57 @@ struct Field {
         return (i0 + p < ns) ? (kRel ? u0_rel(p) : s_u0(sk(i0 + p))) : 0.0;
     }
 
-    __device__ __forceinline__ void phi(const Consts &k, int rk) {
+    // Runge-Kutta stage value of the run's cells from the stage's rhs A
+    // (stepper.py:50-62, Python's left-to-right scalars); the stage is
+    // selected once, outside the cell loop.
+    __device__ __forceinline__ void rk_update(const Consts &k, int rk, int sg, const double *A,
+                                              double *st) {
+        const int code = rk == 0 ? 0 : (sg == 0 ? 1 : (rk == 2 ? 2 : (sg == 1 ? 3 : 4)));
+        switch (code) {
+            case 0:
+#pragma unroll
+                for (int p = 0; p < PC; ++p) st[p] = A[p];
+                break;
+            case 1:
+#pragma unroll
+                for (int p = 0; p < PC; ++p) st[p] = u0(p) + k.dt * A[p];
+                break;
+            case 2:
+#pragma unroll
+                for (int p = 0; p < PC; ++p)
+                    st[p] = ((0.5 * u0(p)) + (0.5 * stage(p))) + (k.hdt * A[p]);
+                break;
+            case 3:
+#pragma unroll
+                for (int p = 0; p < PC; ++p)
+                    st[p] = ((0.75 * u0(p)) + (0.25 * stage(p))) + (k.qdt * A[p]);
+                break;
+            default: {
+                // u0 / 3.0: the reciprocal of 3 refined once for the run
+                // (div_shared.cuh: the compiler's own fast-path sequence and
+                // validity test, IEEE `/` otherwise -- bit-identical to `/`)
+                const SharedRcp R3 = shared_rcp(3.0);
+                bool bad = false;
+                double third[PC];
+#pragma unroll
+                for (int p = 0; p < PC; ++p) third[p] = mgp::div_fast(u0(p), R3, bad);
+                if (bad) {
+#pragma unroll 1
+                    for (int p = 0; p < PC; ++p) third[p] = mgp::div_slow(u0(p), 3.0);
+                }
+#pragma unroll
+                for (int p = 0; p < PC; ++p)
+                    st[p] = (third[p] + (k.two3 * stage(p))) + (k.tdt * A[p]);
+            }
+        }
+    }
+
+    // FUSED: the last stage's values (+ g, sweep_body's add_g for the modes
+    // without an array) are committed straight into s_u with their halo
+    // copies, ready to be the next step's input; otherwise they go to the
+    // result slots (result(t)).
+    template <bool FUSED>
+    __device__ __forceinline__ void phi_t(const Consts &k, int rk, int g_mode) {
 #pragma unroll
         for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) {
@@ -989,24 +1066,25 @@ struct Field {
             double A[PC];
             rhs(k, A);
             double st[PC];
-            const bool last = (sg == stages - 1);
+            rk_update(k, rk, sg, A, st);
+            if (sg < stages - 1) {
+                commit(st);
+            } else if (FUSED) {
+                if (g_mode == MGP_G_ZERO) {
 #pragma unroll
-            for (int p = 0; p < PC; ++p) {
-                if (rk == 0) {
-                    st[p] = A[p];
-                } else if (sg == 0) {
-                    st[p] = u0(p) + k.dt * A[p];
-                } else if (rk == 2) {
-                    st[p] = ((0.5 * u0(p)) + (0.5 * stage(p))) + (k.hdt * A[p]);
-                } else if (sg == 1) {
-                    st[p] = ((0.75 * u0(p)) + (0.25 * stage(p))) + (k.qdt * A[p]);
-                } else {
-                    st[p] = ((u0(p) / 3.0) + (k.two3 * stage(p))) + (k.tdt * A[p]);
+                    for (int p = 0; p < PC; ++p) st[p] = st[p] + 0.0;
                 }
+                commit(st);
+            } else {
+                store_res(st);
             }
-            if (last) store_res(st);
-            else commit(st);
         }
+    }
+    __device__ __forceinline__ void phi(const Consts &k, int rk) {
+        phi_t<false>(k, rk, MGP_G_NONE);
+    }
+    __device__ __forceinline__ void phi_commit(const Consts &k, int rk, int g_mode) {
+        phi_t<true>(k, rk, g_mode);
     }
 
     __device__ __forceinline__ double stage(int p) const {
@@ -1090,8 +1168,43 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
             }
         }
+        // Plain chained steps without a g array: the last stage commits its
+        // state (+ 0.0 per g_mode) straight into s_u (Field::phi_commit);
+        // after the barrier that publishes it, the step's store / error /
+        // non-finite count read it back from s_u in coalesced order while
+        // the next step's reconstruction starts.
+        const bool fused = F::kFusedCommit && a.g_mode != MGP_G_ARRAY && a.phi.repeats == 1;
+        bool pending = false;
+        double *p_st = nullptr;
+        const double *p_rs = nullptr;
+        auto flush = [&]() {
+            if (p_st || p_rs || a.count_nonfinite) {
+                for (int t = tid; t < ns; t += nt) {
+                    const int c = c0 + t;
+                    double v = 0.0;
+                    if constexpr (F::kFusedCommit) v = f.cell(t);
+                    if (p_st) p_st[c] = v;
+                    if (p_rs) {
+                        const double d = v - p_rs[c];
+                        acc_e = acc_e + d * d;
+                    }
+                    if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
+                }
+            }
+            pending = false;
+        };
         for (int s = 1; s <= total; ++s) {
             f.sync();  // s_u and halos complete
+            if (pending) flush();
+            if constexpr (F::kFusedCommit) {
+                if (fused && s <= a.n_steps) {
+                    f.phi_commit(k, rk, a.g_mode);
+                    p_st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
+                    p_rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
+                    pending = true;
+                    continue;
+                }
+            }
             f.phi(k, rk);
             __syncthreads();   // results complete
             // ComposedStepper (stepper.py:170-188): Phi = inner^repeats
@@ -1160,6 +1273,10 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                     }
                 }
             }
+        }
+        if (pending) {
+            f.sync();
+            flush();
         }
         if (a.partials) {
             // fixed-order reduction: warps, CTA, then cluster ranks in order
@@ -1636,18 +1753,30 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
         } else {
             fcf_load(f, rrow, ns, true);
         }
-        for (int st = s0; st < s1; ++st) {
+        // Every step's last stage commits its state straight into s_u (the
+        // next step's input).  After the barrier that publishes it, the
+        // state is flushed from s_u to wherever the step's result goes, in
+        // coalesced order, while the next step's reconstruction starts (s_u
+        // is next written after that step's alpha barrier).
+        double *dst = nullptr, *dst2 = nullptr, *dst3 = nullptr;
+        for (int st = s0; st <= s1; ++st) {
             f.sync();
-            f.phi(k, a.phi.rk_order);
-            __syncthreads();
-            for (int rep = 1; rep < a.phi.repeats; ++rep) {   // ComposedStepper
-                for (int c = tid; c < ns; c += nt) f.put(c, f.result(c));
-                f.sync();
-                f.phi(k, a.phi.rk_order);
-                __syncthreads();
+            if (dst || dst2 || dst3) {
+                for (int c = tid; c < ns; c += nt) {
+                    const double v = f.cell(c);
+                    if (dst) dst[c] = v;
+                    if (dst2) dst2[c] = v;
+                    if (dst3) __stcg(dst3 + c, v);
+                }
             }
+            if (st == s1) break;
+            for (int rep = 1; rep < a.phi.repeats; ++rep) {   // ComposedStepper
+                f.phi_commit(k, a.phi.rk_order, MGP_G_NONE);
+                f.sync();
+            }
+            f.phi_commit(k, a.phi.rk_order, a.g_mode);
             // where this step's state goes
-            double *dst = nullptr, *dst2 = nullptr;
+            dst = dst2 = dst3 = nullptr;
             if (j == pl.nc) {                       // interval 0's final F-steps
                 dst = a.fstore + (int64_t)st * a.f_ss;
             } else if (st == m - 1) {               // C-step: new C-point j+1
@@ -1656,14 +1785,7 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
             } else if (st >= m) {                   // interval j+1's final F-steps
                 dst = a.fstore + (j + 1) * a.f_cs + (int64_t)(st - m) * a.f_ss;
             }
-            const bool hand = seg_mode && (st == s1 - 1) && (s1 < len);   // hand the field on
-            for (int c = tid; c < ns; c += nt) {
-                const double v = add_g(f.result(c), a.g_mode, nullptr, c);
-                f.put(c, v);
-                if (dst) dst[c] = v;
-                if (dst2) dst2[c] = v;
-                if (hand) __stcg(rrow + c, v);
-            }
+            if (seg_mode && (st == s1 - 1) && (s1 < len)) dst3 = rrow;   // hand the field on
         }
         if (seg_mode && s1 < len) {
             __threadfence();   // every thread's row stores before the release
@@ -1723,6 +1845,7 @@ constexpr int kMaxLfNx = 2048;
 template <int MODE>   // 1 = one-step, 2 = matched coarse
 struct LFField {
     static constexpr int HALO = 0;
+    static constexpr bool kFusedCommit = false;
     int ns;
     double *s_u, *s_R, *s_va, *s_vb, *s_aa, *s_ab, *s_f;
 
@@ -1916,6 +2039,7 @@ struct Eig {
 template <int K, bool ROE, int D>
 struct SysField {
     static constexpr int HALO = 0;   // halos are maintained by load/put
+    static constexpr bool kFusedCommit = false;
     static constexpr int H = K;      // window reach
     int nx, pitch;                   // cells; per-component stride of s_u
     bool charwise;                   // characteristic reconstruction
@@ -2583,7 +2707,7 @@ struct FcfLaunch {
 
 template <int K, int P>
 int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
-    auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>;
+    auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, (P == 16 ? 255 : MGP_REGS)>;
     const int ns = (int)phi.nx;
     L.nt = threads_for(ns, P);
     L.smem = smem_bytes(ns, K, 1, P);
@@ -2654,7 +2778,7 @@ int fcf_launch(const mgp_fcf_args &a, cudaStream_t st) {
         pl.R = 0;
         pl.W = pl.nchains + A;
     }
-    fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>
+    fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, (P == 16 ? 255 : MGP_REGS)>
         <<<L.G, L.nt, L.smem, st>>>(a, make_consts(a.phi), pl);
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
@@ -2670,9 +2794,19 @@ bool fcf_supported(const mgp_phi &p, int64_t nc) {
            nc >= 1;
 }
 
+#ifdef MGP_P16   // experiment: runs of 16 cells, 256 threads for 4096 cells
+#define MGP_FCF_P16(KK)                                                 \
+        if (run == 16) return fn(std::integral_constant<int, KK>{},     \
+                                 std::integral_constant<int, 16>{});
+#else
+#define MGP_FCF_P16(KK)
+#endif
 template <class Fn>
 int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
-    const int run = run_length(p.nx, nc > 1 ? nc : 2);
+    int run = run_length(p.nx, nc > 1 ? nc : 2);
+#ifdef MGP_P16
+    if (p.nx >= 4096 && env_int("MGP_RUN") == 16) run = 16;
+#endif
     switch (p.weno_k) {
 #define MGP_FCF_K(KK)                                                   \
     case KK:                                                            \
@@ -2680,6 +2814,7 @@ int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
                                 std::integral_constant<int, 4>{});      \
         if (run == 8) return fn(std::integral_constant<int, KK>{},      \
                                 std::integral_constant<int, 8>{});      \
+        MGP_FCF_P16(KK)                                                 \
         return MGP_EINVAL;
 #ifndef MGP_QUICK
         MGP_FCF_K(0)
