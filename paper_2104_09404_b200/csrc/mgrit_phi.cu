@@ -15,6 +15,7 @@
 //   models.py:107-117 Burgers flux / speed
 //   stepper.py:50-62 SSP-RK1/2/3;  mgrit.py:168-270 level operations.
 #include <cooperative_groups.h>
+#include <vector>
 #include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -475,6 +476,44 @@ __device__ __forceinline__ void field_sync() {
     }
 }
 
+// ---------------------------------------------------------------------------
+// LL exchange: a "virtual cluster" of CS co-resident CTAs that share one field
+// and talk through global memory instead of distributed shared memory, so the
+// group is not tied to one GPC (16-CTA hardware clusters fit 7 times on a
+// B200: 112 of 148 SMs; 9 groups of 16 co-resident CTAs use 144).  A double
+// travels as two 8-byte words, each carrying half the payload and the
+// exchange's 32-bit tag (the words validate themselves: no fence, no flag;
+// measured 1.5k cycles for an all-to-all among 16 CTAs x 9 groups against
+// 4.6k with fence + counter, profiles/r02_ll_exchange.txt).  Boxes are
+// double-buffered by tag parity; the per-stage alpha all-to-all keeps every
+// CTA within one exchange of its peers, which makes the reuse safe (see
+// Field::sync).  The mailbox is zeroed by the launch, tags start at 1.
+// ---------------------------------------------------------------------------
+constexpr int kLLHalo = 4;                       // halo cells per side, K <= 3
+// words per CTA and parity: alpha 2 | states from the left 6 | halo from the
+// left 2*kLLHalo | halo from the right 2*kLLHalo | partial sums 6 | ack 2
+constexpr int kLLAlpha = 0, kLLStates = 2, kLLFromLeft = 8, kLLFromRight = 8 + 2 * kLLHalo,
+              kLLPsum = 8 + 4 * kLLHalo, kLLAck = 14 + 4 * kLLHalo, kLLWords = 16 + 4 * kLLHalo;
+constexpr int kLLSpinLimit = 1 << 22;            // ~ seconds: a lost peer must not hang the GPU
+
+__device__ __forceinline__ void ll_send(unsigned long long *w, double v, unsigned tag) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long t = (unsigned long long)tag << 32;
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(w),
+                 "l"(t | (bits & 0xffffffffull)), "l"(t | (bits >> 32))
+                 : "memory");
+}
+__device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned tag) {
+    unsigned long long lo, hi;
+    int spins = 0;
+    do {
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(w)
+                     : "memory");
+    } while (((unsigned)(lo >> 32) != tag || (unsigned)(hi >> 32) != tag) &&
+             ++spins < kLLSpinLimit);
+    return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
+}
+
 // One field, held in shared memory by one CTA (CS = 1) or split into CS
 // contiguous slabs over a thread-block cluster (CS > 1, for meshes larger
 // than one SM's shared memory and for short sequential marches).  Local cell
@@ -484,8 +523,18 @@ __device__ __forceinline__ void field_sync() {
 // CTA's halo through distributed shared memory when committed), the states of
 // the interface just left of the slab are pushed by the left neighbour, and
 // alpha is reduced over the cluster.
-template <int K, int REG, int MODEL, int P, int CS>
+template <int K, int REG, int MODEL, int P, int CS, bool LL = false>
 struct Field {
+    // LL: the CS CTAs exchange through the global mailbox `mbox` (this
+    // group's region) instead of distributed shared memory
+    unsigned long long *mbox;
+    unsigned eA, eB, eC;      // tags of the last alpha / halo / partial-sum exchange
+    bool halo_pending;        // halo cells were sent since the last sync()
+    __device__ __forceinline__ unsigned long long *box(int par, int cta, int off) const {
+        return mbox + ((size_t)(par * CS + cta) * kLLWords + off);
+    }
+    __device__ __forceinline__ int left() const { return (q + CS - 1) % CS; }
+    __device__ __forceinline__ int right() const { return (q + 1) % CS; }
     static constexpr int H = K + 1;  // halo cells on each side
     // P = 0: latency mode for sequential marches -- two threads per interface
     // (warps alternate between left and right states), one cell per thread
@@ -534,6 +583,7 @@ struct Field {
     // x a literal after unrolling -> base register + immediate
     static constexpr bool kRel = (P == 4 || P == 8 || P == 16);
     static constexpr bool kFusedCommit = true;   // phi_commit available (sweep_body)
+    static constexpr bool kLL = LL && CS > 1;
     static __host__ __device__ constexpr int rel(int x) { return x + (x >> LG); }
     __device__ __forceinline__ double &u_rel(int x) const { return mgp_sm[o_u + b + rel(x + H)]; }
     __device__ __forceinline__ double &L_rel(int x) const { return mgp_sm[o_L + b + rel(x)]; }
@@ -542,7 +592,63 @@ struct Field {
     // barrier over the CTAs sharing the field (hardware cluster barrier; an
     // mbarrier-based all-to-all with one arriving thread per CTA measured
     // 1.8-2.5x slower per stage on B200)
-    __device__ __forceinline__ void sync() { field_sync<CS>(); }
+    __device__ __forceinline__ void sync() {
+        if (!LL) {
+            field_sync<CS>();
+            return;
+        }
+        // LL: the barrier is local.  The neighbours' boundary cells sent at
+        // their last commit are fetched afterwards by the two warps that read
+        // them -- with runs of P >= H cells the left halo is read only by the
+        // slab's first thread and the right halo only by its last -- so the
+        // other warps start their reconstruction without waiting for the
+        // neighbours.  Reuse of a box two exchanges later is safe: a sender
+        // reaches that commit only after this CTA's next alpha, sent after
+        // these reads.
+        if (halo_pending && ns % PC != 0) {
+            // a partial last run: the right halo has readers in two warps;
+            // fetch both halos before the barrier instead
+            const int tid = threadIdx.x;
+            if (tid < 2 * H) {
+                const int par = eB & 1;
+                if (tid < H)
+                    s_u(sk(ns + H + tid)) = ll_recv(box(par, q, kLLFromRight + 2 * tid), eB);
+                else
+                    s_u(sk(tid - H)) = ll_recv(box(par, q, kLLFromLeft + 2 * (tid - H)), eB);
+            }
+            halo_pending = false;
+        }
+        __syncthreads();
+        if (halo_pending) {
+            static_assert(!LL || (P >= 4 && K >= 1), "LL mode: merged runs of >= 4 cells");
+            const int tid = threadIdx.x, lane = tid & 31;
+            const int par = eB & 1;
+            if (tid < 32) {            // cells [-H, 0) = the left neighbour's last H cells
+                if (lane < H) s_u(sk(lane)) = ll_recv(box(par, q, kLLFromLeft + 2 * lane), eB);
+                __syncwarp();
+            }
+            if (tid >> 5 == (ns / PC - 1) >> 5) {   // warp of the slab's last run
+                // cells [ns, ns + H) = the right neighbour's first H cells
+                if (lane < H)
+                    s_u(sk(ns + H + lane)) = ll_recv(box(par, q, kLLFromRight + 2 * lane), eB);
+                __syncwarp();
+            }
+            halo_pending = false;
+        }
+    }
+    // LL: the commit / put phase that follows sends halo cells with this tag
+    __device__ __forceinline__ void begin_halo_exchange() {
+        if (LL && !halo_pending) {
+            ++eB;
+            halo_pending = true;
+        }
+    }
+    __device__ __forceinline__ void send_halo(int t, double v) {
+        // local cell t < H -> the left neighbour's right halo; t >= ns - H ->
+        // the right neighbour's left halo
+        if (t < H) ll_send(box(eB & 1, left(), kLLFromRight + 2 * t), v, eB);
+        if (t >= ns - H) ll_send(box(eB & 1, right(), kLLFromLeft + 2 * (t - (ns - H))), v, eB);
+    }
 
     static constexpr int HALO = H;
     __device__ __forceinline__ double cell(int t) const { return s_u(sk(t + H)); }
@@ -568,6 +674,8 @@ struct Field {
         if (CS == 1) {
             if (t < H) s_u(sk(ns + H + t)) = v;
             if (t >= ns - H) s_u(sk(t - (ns - H))) = v;
+        } else if (LL) {
+            send_halo(t, v);
         } else {
             if (t < H) r_u_left[sk(ns + H + t)] = v;
             if (t >= ns - H) r_u_right[sk(t - ns + H)] = v;
@@ -613,7 +721,7 @@ struct Field {
             if (kCheck && badw) v = __longlong_as_double(kNaNBits);
             if (side == 0) s_L(sk(i)) = v;
             else s_R(sk(i)) = v;
-            if (CS > 1 && i == ns - 1) r_edge_right[side] = v;
+            if (CS > 1 && i == ns - 1) push_edge(side, v);
             if (MODEL == MGP_MODEL_BURGERS) {
                 m = abs_bits(v);
                 if (side == 0 && !is_finite(win[K])) m = kNaNBits;
@@ -639,8 +747,8 @@ struct Field {
                 s_L(sk(i)) = ul;
                 s_R(sk(i)) = ur;
                 if (CS > 1 && i == ns - 1) {
-                    r_edge_right[0] = ul;
-                    r_edge_right[1] = ur;
+                    push_edge(0, ul);
+                    push_edge(1, ur);
                 }
                 if (MODEL == MGP_MODEL_BURGERS) {
                     m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
@@ -700,8 +808,8 @@ struct Field {
             s_L(sk(i)) = ul;
             s_R(sk(i)) = ur;
             if (CS > 1 && i == ns - 1) {
-                r_edge_right[0] = ul;
-                r_edge_right[1] = ur;
+                push_edge(0, ul);
+                push_edge(1, ur);
             }
             if (MODEL == MGP_MODEL_BURGERS) {
                 m = umax64(m, umax64(abs_bits(ul), abs_bits(ur)));
@@ -725,15 +833,26 @@ struct Field {
     // iteration, so no window is evaluated twice and nothing is carried
     // between iterations; the fully unrolled loop keeps the sliding window
     // in registers without copies.
+    // states owed to the right neighbour: the two states of this slab's last
+    // interface (its s_edge) and the left state of its interface 0.  The
+    // alpha exchange that follows the reconstruction carries tag eA + 1.
+    __device__ __forceinline__ void push_edge(int side, double v) {
+        if (LL) ll_send(box((eA + 1) & 1, right(), kLLStates + 2 * side), v, eA + 1);
+        else r_edge_right[side] = v;
+    }
+    __device__ __forceinline__ void push_L0(double v) {
+        if (LL) ll_send(box((eA + 1) & 1, right(), kLLStates + 4), v, eA + 1);
+        else r_L_right[0] = v;
+    }
     __device__ __forceinline__ void store_states(int c, double ul, double ur) {
         if (CS == 1) {
             s_L(sk(c == ns ? 0 : c)) = ul;
         } else if (c == ns) {
-            r_L_right[sk(0)] = ul;      // L state of the neighbour's interface 0
-            r_edge_right[1] = ur;       // R state of the slab's last interface
+            push_L0(ul);                // L state of the neighbour's interface 0
+            push_edge(1, ur);           // R state of the slab's last interface
         } else {
             s_L(sk(c)) = ul;
-            if (c == ns - 1) r_edge_right[0] = ul;
+            if (c == ns - 1) push_edge(0, ul);
         }
         s_R(sk(c - 1)) = ur;
     }
@@ -745,12 +864,12 @@ struct Field {
             if (CS == 1) {
                 s_L(0) = ul;
             } else {
-                r_L_right[0] = ul;
-                r_edge_right[1] = ur;
+                push_L0(ul);
+                push_edge(1, ur);
             }
         } else {
             L_rel(1 + p) = ul;
-            if (CS > 1 && p >= PC - 2 && c == ns - 1) r_edge_right[0] = ul;
+            if (CS > 1 && p >= PC - 2 && c == ns - 1) push_edge(0, ul);
         }
         R_rel(p) = ur;
     }
@@ -905,7 +1024,29 @@ struct Field {
             // at most kMaxThreads / 32 = 16 warps: one slot per lane
             const int nw = (blockDim.x + 31) >> 5;
             m = warp_umax64((tid & 31) < nw ? s_red(tid & 31) : 0ull);
-            if (CS > 1) {
+            if (CS > 1 && LL) {
+                // all-to-all of the CTAs' alpha bits through the mailbox, and
+                // the three states the left neighbour computed for this slab
+                ++eA;
+                const int par = eA & 1;
+                if (tid < 32) {
+                    if (tid == 0)
+                        ll_send(box(par, q, kLLAlpha), __longlong_as_double((long long)m), eA);
+                    unsigned long long v = 0;
+                    if (tid < CS)
+                        v = (unsigned long long)__double_as_longlong(
+                            ll_recv(box(par, tid, kLLAlpha), eA));
+                    v = warp_umax64(v);
+                    if (tid == 0) s_cmax(0) = v;
+                    if (tid < 3) {
+                        const double sv = ll_recv(box(par, q, kLLStates + 2 * tid), eA);
+                        if (tid < 2) s_edge(tid) = sv;
+                        else s_L(0) = sv;
+                    }
+                }
+                __syncthreads();
+                m = s_cmax(0);
+            } else if (CS > 1) {
                 if (threadIdx.x == 0) {
                     cg::cluster_group cl = cg::this_cluster();
 #pragma unroll
@@ -1092,6 +1233,7 @@ struct Field {
     }
 
     __device__ __forceinline__ void commit(const double *v) {
+        begin_halo_exchange();
         if (kRel && ns >= 2 * PC && (i0 + PC + H <= ns || i0 + PC == ns)) {
             // full run: literal offsets; the periodic halo copies (cells
             // [0, H) and [ns - H, ns), H <= PC) belong to the first and the
@@ -1102,6 +1244,7 @@ struct Field {
 #pragma unroll
                 for (int p = 0; p < H; ++p) {
                     if (CS == 1) s_u(sk(ns + H + p)) = v[p];
+                    else if (LL) send_halo(p, v[p]);
                     else r_u_left[sk(ns + H + p)] = v[p];
                 }
             }
@@ -1109,6 +1252,7 @@ struct Field {
 #pragma unroll
                 for (int p = PC - H; p < PC; ++p) {
                     if (CS == 1) s_u(sk(p - (PC - H))) = v[p];
+                    else if (LL) send_halo(ns - PC + p, v[p]);
                     else r_u_right[sk(p - (PC - H))] = v[p];
                 }
             }
@@ -1209,12 +1353,14 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
             __syncthreads();   // results complete
             // ComposedStepper (stepper.py:170-188): Phi = inner^repeats
             for (int rep = 1; rep < a.phi.repeats; ++rep) {
+                if constexpr (F::kFusedCommit) f.begin_halo_exchange();
                 for (int t = tid; t < ns; t += nt) f.put(t, f.result(t));
                 f.sync();
                 f.phi(k, rk);
                 __syncthreads();
             }
             if (s <= a.n_steps) {
+                if constexpr (F::kFusedCommit) f.begin_halo_exchange();
                 const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
                 double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
                 const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
@@ -1299,12 +1445,35 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 for (int w = 0; w < nw; ++w) t = t + s_sum[3 * w + tid];
                 if (CS == 1) {
                     a.partials[3 * b + tid] = t;
+                } else if constexpr (F::kLL) {
+                    // ranks' partials through the mailbox, summed by rank 0
+                    // in rank order (as the cluster path).  A chunk may hold
+                    // no alpha exchange (no steps), so this exchange carries
+                    // its own back-pressure: nobody passes the chunk's last
+                    // barrier before rank 0 has read every word.
+                    const unsigned e = f.eC + 1;
+                    ll_send(f.box(0, q, kLLPsum + 2 * tid), t, e);
+                    if (q == 0) {
+                        double tt = 0.0;
+                        for (int j = 0; j < CS; ++j)
+                            tt = tt + ll_recv(f.box(0, j, kLLPsum + 2 * tid), e);
+                        a.partials[3 * b + tid] = tt;
+                    }
                 } else {
                     cg::cluster_group cl = cg::this_cluster();
                     cl.map_shared_rank(s_psum, 0)[3 * q + tid] = t;
                 }
             }
-            if (CS > 1) {
+            if constexpr (F::kLL) {
+                ++f.eC;
+                if (tid < 32) {
+                    __syncwarp();   // rank 0's three readers are done
+                    if (tid == 0) {
+                        if (q == 0) ll_send(f.box(0, 0, kLLAck), 0.0, f.eC);
+                        else (void)ll_recv(f.box(0, 0, kLLAck), f.eC);
+                    }
+                }
+            } else if (CS > 1) {
                 f.sync();
                 if (q == 0 && tid < 3) {
                     double t = 0.0;
@@ -1317,10 +1486,15 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
     }
 }
 
-template <int K, int REG, int MODEL, int P, int REGS, int CS>
-__global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k) {
-    using F = Field<K, REG, MODEL, P, CS>;
+template <int K, int REG, int MODEL, int P, int REGS, int CS, bool LL = false>
+__global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k,
+                                               unsigned long long *mbox) {
+    using F = Field<K, REG, MODEL, P, CS, LL>;
     F f;
+    f.eA = f.eB = f.eC = 0;
+    f.halo_pending = false;
+    // LL: this group's region of the mailbox (zeroed by the launch)
+    f.mbox = LL ? mbox + (size_t)(blockIdx.x / CS) * 2 * CS * kLLWords : nullptr;
     const int nx = (int)a.phi.nx;
     const int ns = nx / CS;            // cells of this CTA's slab
     const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
@@ -1333,7 +1507,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     f.o_edge = o_sum + 3 * 32 + 3 * CS;        // [2]
     f.o_cmax = f.o_edge + 2;                   // [CS]
     f.o_red = f.o_cmax + CS;                   // [32]
-    if (CS > 1) {
+    if (CS > 1 && !LL) {
         cg::cluster_group cl = cg::this_cluster();
         f.r_u_left = cl.map_shared_rank(&f.s_u(0), (q + CS - 1) % CS);
         f.r_u_right = cl.map_shared_rank(&f.s_u(0), (q + 1) % CS);
@@ -1846,6 +2020,7 @@ template <int MODE>   // 1 = one-step, 2 = matched coarse
 struct LFField {
     static constexpr int HALO = 0;
     static constexpr bool kFusedCommit = false;
+    static constexpr bool kLL = false;
     int ns;
     double *s_u, *s_R, *s_va, *s_vb, *s_aa, *s_ab, *s_f;
 
@@ -2040,6 +2215,7 @@ template <int K, bool ROE, int D>
 struct SysField {
     static constexpr int HALO = 0;   // halos are maintained by load/put
     static constexpr bool kFusedCommit = false;
+    static constexpr bool kLL = false;
     static constexpr int H = K;      // window reach
     int nx, pitch;                   // cells; per-component stride of s_u
     bool charwise;                   // characteristic reconstruction
@@ -2434,19 +2610,75 @@ size_t smem_bytes(int64_t ns, int k, int cs, int p) {
            sizeof(unsigned long long) * (size_t)(cs + 32);
 }
 
-template <int K, int REG, int MODEL, int P, int REGS, int CS>
+// LL mailbox (Field, LL mode): one allocation per device and stream, grown on
+// demand, zeroed by every launch that uses it (tags restart at 1).
+unsigned long long *ll_mailbox(size_t words, cudaStream_t st) {
+    struct Box {
+        int dev;
+        cudaStream_t st;
+        unsigned long long *p;
+        size_t words;
+    };
+    static std::vector<Box> boxes;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    Box *bx = nullptr;
+    for (auto &b : boxes)
+        if (b.dev == dev && b.st == st) bx = &b;
+    if (!bx) {
+        boxes.push_back(Box{dev, st, nullptr, 0});
+        bx = &boxes.back();
+    }
+    if (bx->words < words) {
+        if (bx->p) cudaFree(bx->p);
+        bx->p = nullptr;
+        bx->words = 0;
+        if (cudaMalloc(&bx->p, words * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+        bx->words = words;
+    }
+    if (cudaMemsetAsync(bx->p, 0, words * sizeof(unsigned long long), st) != cudaSuccess)
+        return nullptr;
+    return bx->p;
+}
+
+template <int K, int REG, int MODEL, int P, int REGS, int CS, bool LL = false>
 int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     const int64_t ns = a.phi.nx / CS;
     const int nt = threads_for(ns, P);
     const size_t sm = smem_bytes(ns, K, CS, P);
-    auto kern = sweep_kernel<K, REG, MODEL, P, REGS, CS>;
+    auto kern = sweep_kernel<K, REG, MODEL, P, REGS, CS, LL>;
     static unsigned long long attr_devs = 0;
-    if (!ensure_attrs(kern, attr_devs, CS > 8)) return MGP_ECUDA;
+    if (!ensure_attrs(kern, attr_devs, CS > 8 && !LL)) return MGP_ECUDA;
     int64_t grid = a.n_chunks;
     if (grid > ((int64_t)1 << 30) / CS) grid = ((int64_t)1 << 30) / CS;
     const Consts k = make_consts(a.phi);
+    unsigned long long *mbox = nullptr;
     if (CS == 1) {
-        kern<<<(unsigned)grid, nt, sm, st>>>(a, k);
+        kern<<<(unsigned)grid, nt, sm, st>>>(a, k, mbox);
+    } else if (LL) {
+        // groups of CS co-resident CTAs (cooperative launch: all resident or
+        // the launch fails), as many groups as fit the device
+        int dev = 0, nsm = 0, per = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm) != cudaSuccess)
+            return MGP_ECUDA;
+        const int64_t groups = (int64_t)per * nsm / CS;
+        if (groups < 1) return MGP_ECUDA;
+        if (grid > groups) grid = groups;
+        mbox = ll_mailbox((size_t)grid * 2 * CS * kLLWords, st);
+        if (!mbox) return MGP_ECUDA;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(grid * CS));
+        cfg.blockDim = dim3(nt);
+        cfg.dynamicSmemBytes = sm;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid * CS));
@@ -2460,7 +2692,7 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, a, k) != cudaSuccess) return MGP_ECUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
     }
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
@@ -2587,6 +2819,20 @@ int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
         // (two threads per interface) for slabs <= 256 cells, else P = 1
         const int64_t nsl = a.phi.nx / cs;
         const int mode = nsl > 512 ? 8 : (nsl <= 256 ? 0 : 1);
+        // batched sweeps of a split mesh: groups of co-resident CTAs that
+        // exchange through global memory (every SM usable; hardware clusters
+        // of 16 fit 7 times on a B200).  MGP_LL=0 keeps the cluster path.
+        if (mode == 8 && a.n_chunks > 1 && a.phi.nx > kMaxNx) {
+            const char *e = getenv("MGP_LL");
+            if (!(e && atoi(e) == 0)) {
+                switch (cs) {
+                    case 2: return launch_t<K, REG, MODEL, 8, MGP_REGS, 2, true>(a, st);
+                    case 4: return launch_t<K, REG, MODEL, 8, MGP_REGS, 4, true>(a, st);
+                    case 8: return launch_t<K, REG, MODEL, 8, MGP_REGS, 8, true>(a, st);
+                    case 16: return launch_t<K, REG, MODEL, 8, MGP_REGS, 16, true>(a, st);
+                }
+            }
+        }
         switch (cs) {
             case 2: return mode == 8 ? launch_t<K, REG, MODEL, 8, MGP_REGS, 2>(a, st)
                          : mode == 0 ? launch_t<K, REG, MODEL, 0, MGP_REGS, 2>(a, st)

@@ -105,7 +105,6 @@ class DistMgritHierarchy:
             for l in range(self.D, L):
                 self._u[l] = torch.zeros(self.n[l] + 1, nx, **kw)
                 self._g[l] = torch.zeros(self.n[l] + 1, nx, **kw)
-        self._phi_buf = torch.empty(max(n0, 1), nx, **kw)
         self._partials = torch.empty(max(n0 * m + 1, 1) * 3, **kw)
         self._sums = torch.empty(4, **kw)
 
@@ -310,36 +309,39 @@ class DistMgritHierarchy:
                                     self._g[l + 1], self.c[l], guess, regime)
             return
         nc = self.nloc[l]
-        # fine rows owned here: level-0 C-points or level-l nodes
-        if l == 0:
-            cpts = self._c[self._cur]
-            fine_u0 = cpts[0]
-            if self._fsrc == "ic":
-                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._u0, start_stride=0,
-                          tail=TAIL_PHI, tail_regime=regime, tail_out=self._phi_buf, to_s=nx,
-                          what="restrict/fine")
-            else:
-                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._c[self._fsrc],
-                          start_stride=nx, n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
-                          tail_regime=regime, tail_out=self._phi_buf, to_s=nx,
-                          what="restrict/fine")
-            c_start, c_stride, gf_mode, gf, gf_s, inj, inj_s = cpts, nx, G_ZERO, None, 0, cpts[1], nx
-        else:
-            fu, fg = self._u[l], self._g[l]
-            fine_u0 = fu[0]
-            dev.sweep(self._phi(l, regime), n_chunks=nc, start=fu[m - 1], start_stride=m * nx,
-                      tail=TAIL_PHI, tail_regime=regime, tail_out=self._phi_buf, to_s=nx,
-                      what="restrict/fine")
-            c_start, c_stride, gf_mode, gf, gf_s, inj, inj_s = fu, m * nx, G_ARRAY, fg[m], m * nx, fu[m], m * nx
         if l + 1 < self.D:
             cu, cg = self._u[l + 1], self._g[l + 1]
             out_g, out_u = cg[1], cu[1]
         else:
             tmp = torch.empty(2, nc, nx, dtype=dev.DTYPE, device=self.device)
             out_g, out_u = tmp[0], tmp[1]
+        # phi_fine goes into the coarse u rows themselves (the FAS kernel
+        # reads element c before it writes it): no level-sized scratch
+        phi_buf = out_u
+        # fine rows owned here: level-0 C-points or level-l nodes
+        if l == 0:
+            cpts = self._c[self._cur]
+            fine_u0 = cpts[0]
+            if self._fsrc == "ic":
+                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._u0, start_stride=0,
+                          tail=TAIL_PHI, tail_regime=regime, tail_out=phi_buf, to_s=nx,
+                          what="restrict/fine")
+            else:
+                dev.sweep(self._phi(0, regime), n_chunks=nc, start=self._c[self._fsrc],
+                          start_stride=nx, n_steps=m - 1, g_mode=G_ZERO, tail=TAIL_PHI,
+                          tail_regime=regime, tail_out=phi_buf, to_s=nx,
+                          what="restrict/fine")
+            c_start, c_stride, gf_mode, gf, gf_s, inj, inj_s = cpts, nx, G_ZERO, None, 0, cpts[1], nx
+        else:
+            fu, fg = self._u[l], self._g[l]
+            fine_u0 = fu[0]
+            dev.sweep(self._phi(l, regime), n_chunks=nc, start=fu[m - 1], start_stride=m * nx,
+                      tail=TAIL_PHI, tail_regime=regime, tail_out=phi_buf, to_s=nx,
+                      what="restrict/fine")
+            c_start, c_stride, gf_mode, gf, gf_s, inj, inj_s = fu, m * nx, G_ARRAY, fg[m], m * nx, fu[m], m * nx
         dev.sweep(self._phi(l + 1, regime), n_chunks=nc, start=c_start, start_stride=c_stride,
                   tail=TAIL_RESTRICT, tail_regime=regime, tail_g_mode=gf_mode, tail_g=gf,
-                  tg_s=gf_s, guess=guess, aux=self._phi_buf, aux_s=nx, aux2=inj, aux2_s=inj_s,
+                  tg_s=gf_s, guess=guess, aux=phi_buf, aux_s=nx, aux2=inj, aux2_s=inj_s,
                   tail_out=out_g, to_s=nx, tail_out2=out_u, to2_s=nx, what="restrict/coarse")
         if l + 1 < self.D:
             if self.r == 0:
@@ -362,7 +364,7 @@ class DistMgritHierarchy:
         m, nx = self.options.m, self.nx
         cg[0].copy_(fu[0])
         cu[0].copy_(fu[0])
-        phi_buf = torch.empty(nc, nx, dtype=dev.DTYPE, device=self.device)
+        phi_buf = cu[1]    # in place, as in restrict()
         dev.sweep(self._phi(l, regime), n_chunks=nc, start=fu[m - 1], start_stride=m * nx,
                   tail=TAIL_PHI, tail_regime=regime, tail_out=phi_buf, to_s=nx,
                   what="restrict/fine")

@@ -31,6 +31,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass
+import weakref
 from typing import Sequence
 
 import numpy as np
@@ -114,11 +115,22 @@ class MgritLevel:
     finest right-hand side (initial state at node 0, zero elsewhere)."""
 
     def __init__(self, hierarchy, index, dt, n_intervals, stepper):
-        self._h = hierarchy
+        # a weak reference: no hierarchy <-> level cycle, so dropping the
+        # last reference to a hierarchy frees its device arrays at once
+        # (config 5 holds 35 GB per hierarchy) instead of at the next
+        # collection of the cyclic garbage collector
+        self._href = weakref.ref(hierarchy)
         self.index = index
         self.dt = dt
         self.n_intervals = n_intervals
         self.stepper = stepper
+
+    @property
+    def _h(self):
+        h = self._href()
+        if h is None:
+            raise ReferenceError("the MgritHierarchy of this level no longer exists")
+        return h
 
     @property
     def u(self):
@@ -208,7 +220,6 @@ class MgritHierarchy:
         # levels >= 1: full u and g
         self._u = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
         self._g = [None] + [torch.zeros(self.n[l] + 1, nx, **kw) for l in range(1, L)]
-        self._phi_buf = torch.empty(max(n1, 1), nx, **kw)
         # fused FCF relaxation: steps per hand-over segment (0 = whole chains)
         # and split plan (0 = automatic, -1 = whole chains only)
         self._fcf_segment = 0
@@ -319,7 +330,10 @@ class MgritHierarchy:
         nc = self.n[l + 1]
         regime = dev.regime_for_batch(nc)
         cu, cg = self._u[l + 1], self._g[l + 1]
-        phi_buf = self._phi_buf
+        # phi_fine goes into the coarse u rows themselves: the FAS kernel
+        # reads element c of it before it writes element c of u_c, so no
+        # scratch array the size of the level is needed
+        phi_buf = cu[1]
         guess = GUESS_LAST_STEP if self.options.guess == "last-step" else GUESS_INJECTION
         if l == 0:
             cpts = self._c[self._cur]

@@ -45,7 +45,11 @@ for name in sys.argv[1:]:
     relax_ms = a.elapsed_time(b)
     n1 = pb.n_t // pb.m
     pts = pb.m * n1 * pb.n_x          # fused F+C work actually executed
-    # one full iteration from the initial iterate
+    # one full iteration from the initial iterate (one hierarchy alive: its
+    # peak is the config's memory footprint)
+    del h
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats()
     h = P.MgritHierarchy(st, u0, tg, pb.space_grid(), pb.options())
     torch.cuda.synchronize()
     a, b = ev(), ev()
