@@ -1142,6 +1142,18 @@ struct Field {
     // Runge-Kutta stage value of the run's cells from the stage's rhs A
     // (stepper.py:50-62, Python's left-to-right scalars); the stage is
     // selected once, outside the cell loop.
+    // FULL: a full run addressed by literal offsets (no per-cell range test)
+    template <bool FULL>
+    __device__ __forceinline__ double u0v(int p) const {
+        if (FULL) return u0_rel(p);
+        return u0(p);
+    }
+    template <bool FULL>
+    __device__ __forceinline__ double stv(int p) const {
+        if (FULL) return u_rel(p);
+        return stage(p);
+    }
+    template <bool FULL = false>
     __device__ __forceinline__ void rk_update(const Consts &k, int rk, int sg, const double *A,
                                               double *st) {
         const int code = rk == 0 ? 0 : (sg == 0 ? 1 : (rk == 2 ? 2 : (sg == 1 ? 3 : 4)));
@@ -1152,17 +1164,17 @@ struct Field {
                 break;
             case 1:
 #pragma unroll
-                for (int p = 0; p < PC; ++p) st[p] = u0(p) + k.dt * A[p];
+                for (int p = 0; p < PC; ++p) st[p] = u0v<FULL>(p) + k.dt * A[p];
                 break;
             case 2:
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
-                    st[p] = ((0.5 * u0(p)) + (0.5 * stage(p))) + (k.hdt * A[p]);
+                    st[p] = ((0.5 * u0v<FULL>(p)) + (0.5 * stv<FULL>(p))) + (k.hdt * A[p]);
                 break;
             case 3:
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
-                    st[p] = ((0.75 * u0(p)) + (0.25 * stage(p))) + (k.qdt * A[p]);
+                    st[p] = ((0.75 * u0v<FULL>(p)) + (0.25 * stv<FULL>(p))) + (k.qdt * A[p]);
                 break;
             default: {
                 // u0 / 3.0: the reciprocal of 3 refined once for the run
@@ -1172,14 +1184,14 @@ struct Field {
                 bool bad = false;
                 double third[PC];
 #pragma unroll
-                for (int p = 0; p < PC; ++p) third[p] = mgp::div_fast(u0(p), R3, bad);
+                for (int p = 0; p < PC; ++p) third[p] = mgp::div_fast(u0v<FULL>(p), R3, bad);
                 if (bad) {
 #pragma unroll 1
-                    for (int p = 0; p < PC; ++p) third[p] = mgp::div_slow(u0(p), 3.0);
+                    for (int p = 0; p < PC; ++p) third[p] = mgp::div_slow(u0v<FULL>(p), 3.0);
                 }
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
-                    st[p] = (third[p] + (k.two3 * stage(p))) + (k.tdt * A[p]);
+                    st[p] = (third[p] + (k.two3 * stv<FULL>(p))) + (k.tdt * A[p]);
             }
         }
     }
@@ -1207,7 +1219,8 @@ struct Field {
             double A[PC];
             rhs(k, A);
             double st[PC];
-            rk_update(k, rk, sg, A, st);
+            if (kMerged && kRel && i0 + PC <= ns) rk_update<true>(k, rk, sg, A, st);
+            else rk_update<false>(k, rk, sg, A, st);
             if (sg < stages - 1) {
                 commit(st);
             } else if (FUSED) {
@@ -1536,8 +1549,37 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
 // Same arithmetic as Field::phi + sweep_body (bit-identical); used for
 // plain marches (no tail, no partial sums, no repeats).
 // ---------------------------------------------------------------------------
+// Exchange primitive of the march (round 2): the pushed interface states and
+// alpha slots travel as st.async stores that complete on the RECEIVER's
+// mbarrier (complete_tx), and every thread of the receiver arrives on the same
+// mbarrier after its own shared-memory stores -- so one mbarrier phase per
+// stage and CTA replaces the cluster barrier.  A cluster-scope release
+// compiles to MEMBAR.ALL.GPU on sm_100a (it waited for the acknowledgement of
+// every pushed word: 1.57 `membar` stalls per issue in round 1's ncu); the
+// mbarrier needs none.  MGP_MARCH_CLSYNC builds the cluster-barrier variant.
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned mapa_u32(unsigned addr, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_b64(unsigned raddr, unsigned long long v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                     raddr),
+                 "l"(v), "r"(rbar)
+                 : "memory");
+}
+
 template <int K, int REG, int CS>
 __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, const Consts k) {
+#ifdef MGP_MARCH_CLSYNC
+    constexpr bool kAsync = false;
+#else
+    constexpr bool kAsync = true;
+#endif
+    __shared__ alignas(8) unsigned long long s_mbar[2];   // one per stage parity
     constexpr int G = K + 1;   // ghost cells per side
     constexpr int IL = G + 1;  // interfaces held left of the slab: local [-IL, -1]
     constexpr int IR = G;      // and right of it: [ns, ns + IR)
@@ -1571,7 +1613,24 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
         s_u0[t + G] = v;
         s_v[t + G] = v;
     }
-    cl.sync();   // every CTA of the cluster running and loaded
+    // st.async targets: the neighbours' state arrays and mbarriers, every
+    // CTA's alpha slots and mbarriers (lane j < CS addresses CTA j)
+    const unsigned a_L = smem_u32(s_L), a_R = smem_u32(s_R), a_am = smem_u32(s_am);
+    const unsigned a_bar = smem_u32(s_mbar);
+    const int ql = (q + CS - 1) % CS, qr = (q + 1) % CS;
+    const unsigned al_L = mapa_u32(a_L, ql), al_R = mapa_u32(a_R, ql), al_bar = mapa_u32(a_bar, ql);
+    const unsigned ar_L = mapa_u32(a_L, qr), ar_R = mapa_u32(a_R, qr), ar_bar = mapa_u32(a_bar, qr);
+    const unsigned aj_am = mapa_u32(a_am, lane < CS ? lane : 0);
+    const unsigned aj_bar = mapa_u32(a_bar, lane < CS ? lane : 0);
+    if (kAsync && tid == 0) {
+        for (int p2 = 0; p2 < 2; ++p2)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a_bar + 8 * p2), "r"(nt));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl.sync();   // every CTA of the cluster running, loaded, mbarriers initialised
+    // bytes a CTA receives per stage: 2 IL states from the left neighbour,
+    // 2 IR from the right one, CS * nw alpha slots
+    const unsigned tx_bytes = 8u * (unsigned)(2 * IL + 2 * IR + CS * nw);
 
     const int side = warp & 1;                     // warp-uniform
     const int i = ((warp >> 1) << 5) + lane;       // interface i + 1/2 (local)
@@ -1583,6 +1642,7 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
     const int rk = a.phi.rk_order;
     const int stages = rk == 0 ? 1 : rk;
     int par = 0;
+    int stage_no = 0;        // stages completed: parity par, mbarrier phase (stage_no >> 1) & 1
 #ifdef MGP_TRACE
     long long prof[6] = {0, 0, 0, 0, 0, 0}, pt0 = clock64(), pt1;
 #define MARCH_PROF(ph) do { pt1 = clock64(); prof[ph] += pt1 - pt0; pt0 = pt1; } while (0)
@@ -1630,17 +1690,55 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
                 }
                 const int o = par * ni;
                 (side == 0 ? L : R)[i + IL] = v;
-                if (i < IR) (side == 0 ? rl_L : rl_R)[o + ns + i + IL] = v;
-                if (i >= ns - IL) (side == 0 ? rr_L : rr_R)[o + i - ns + IL] = v;
+                if (kAsync) {
+                    const unsigned long long vb = (unsigned long long)__double_as_longlong(v);
+                    if (i < IR)
+                        st_async_b64((side == 0 ? al_L : al_R) + 8u * (unsigned)(o + ns + i + IL),
+                                     vb, al_bar + 8 * par);
+                    if (i >= ns - IL)
+                        st_async_b64((side == 0 ? ar_L : ar_R) + 8u * (unsigned)(o + i - ns + IL),
+                                     vb, ar_bar + 8 * par);
+                } else {
+                    if (i < IR) (side == 0 ? rl_L : rl_R)[o + ns + i + IL] = v;
+                    if (i >= ns - IL) (side == 0 ? rr_L : rr_R)[o + i - ns + IL] = v;
+                }
                 m = abs_bits(v);
                 // a non-finite cell makes the reference's alpha NaN
                 if (side == 0 && !is_finite(win[K])) m = kNaNBits;
             }
             MARCH_PROF(0);
             m = warp_umax64(m);
-            if (lane < CS) r_am[par * CS * nw + q * nw + warp] = m;
-            MARCH_PROF(1);
-            cl.sync();   // release / acquire: states, ghosts' interfaces, alpha slots
+            if (kAsync) {
+                if (lane < CS)
+                    st_async_b64(aj_am + 8u * (unsigned)(par * CS * nw + q * nw + warp), m,
+                                 aj_bar + 8 * par);
+                MARCH_PROF(1);
+                // every thread arrives (release: its own shared-memory stores)
+                // and waits for the phase: all local arrivals + all pushed bytes
+                if (tid == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                                     a_bar + 8 * par),
+                                 "r"(tx_bytes)
+                                 : "memory");
+                else
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a_bar + 8 * par)
+                                 : "memory");
+                const unsigned phase = (unsigned)(stage_no >> 1) & 1u;
+                unsigned done = 0;
+                while (!done)
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                        "selp.u32 %0, 1, 0, p;\n\t}"
+                        : "=r"(done)
+                        : "r"(a_bar + 8 * par), "r"(phase)
+                        : "memory");
+                ++stage_no;
+            } else {
+                if (lane < CS) r_am[par * CS * nw + q * nw + warp] = m;
+                MARCH_PROF(1);
+                cl.sync();   // release / acquire: states, ghosts' interfaces, alpha slots
+            }
             MARCH_PROF(2);
             unsigned long long mm = 0;
             for (int l = lane; l < CS * nw; l += 32) mm = umax64(mm, s_am[par * CS * nw + l]);
@@ -1678,6 +1776,7 @@ __global__ void __launch_bounds__(512, 1) march_kernel(const mgp_sweep_args a, c
             MARCH_PROF(5);
         }
     }
+    if (kAsync) cl.sync();   // no CTA leaves while a peer's pushes may be in flight
 #ifdef MGP_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int ph = 0; ph < 6; ++ph) {
@@ -1944,11 +2043,13 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
                 }
             }
             if (st == s1) break;
-            for (int rep = 1; rep < a.phi.repeats; ++rep) {   // ComposedStepper
-                f.phi_commit(k, a.phi.rk_order, MGP_G_NONE);
-                f.sync();
+            // ComposedStepper: Phi = inner^repeats, + g after the last (one
+            // call site: the propagator's code exists once in the kernel)
+#pragma unroll 1
+            for (int rep = a.phi.repeats; rep > 0; --rep) {
+                f.phi_commit(k, a.phi.rk_order, rep == 1 ? a.g_mode : MGP_G_NONE);
+                if (rep > 1) f.sync();
             }
-            f.phi_commit(k, a.phi.rk_order, a.g_mode);
             // where this step's state goes
             dst = dst2 = dst3 = nullptr;
             if (j == pl.nc) {                       // interval 0's final F-steps
