@@ -2838,21 +2838,24 @@ int cluster_size(const mgp_sweep_args &a) {
     return 1;
 }
 
-// Cluster size of the one-barrier-per-stage march (march_kernel), or 0 when
+// Cluster size of the one-exchange-per-stage march (march_kernel), or 0 when
 // the call is not a plain single-field march it covers (Burgers RK-WENO,
-// WENO1/3/5).  Slabs of >= 64 cells (first order: 128; MGP_MARCH_MIN_SLAB),
-// at most 16 CTAs and 256 cells per CTA.  Measured on B200, us per SSP-RK3
-// step (profiles/r01_march2.txt), Field path -> march_kernel:
-//   WENO5 nx 512  4.99 -> 3.32 (8 CTAs)   nx 1024 5.89 -> 3.73 (16)  nx 4096 9.0 -> 6.29 (16)
-//   WENO3 nx 512  4.25 -> 3.05 (8)        nx 1024 6.91 -> 3.36 (16)  nx 4096 20.1 -> 5.24 (16)
-//   WENO1 nx 512  3.22 -> 2.31 (4)        nx 1024 4.01 -> 2.76 (8)   nx 4096 11.2 -> 4.63 (16)
-// MGP_MARCH_CS forces the size, MGP_MARCH2=0 selects the Field path.
+// WENO1/3/5).  At most 16 CTAs and 256 cells per CTA.  Measured on B200 with
+// the st.async / mbarrier exchange, us per SSP-RK3 step
+// (profiles/r02_march_async.txt; round 1's cluster-barrier exchange in
+// brackets), Field path -> best march_kernel cluster:
+//   WENO5 nx 128  4.04 -> 2.20 (2 CTAs)   nx 512 4.67 -> 2.43 (16) [3.32]   nx 4096 7.97 -> 5.01 (16) [6.29]
+//   WENO3 nx 128  2.10 -> 1.87 (2)        nx 512 3.54 -> 2.19 (16) [3.05]   nx 4096 15.4 -> 4.09 (16) [5.24]
+//   WENO1 nx 128  1.61 -> 1.39 (2)        nx 512 2.10 -> 1.68 (16) [2.31]   nx 4096 9.79 -> 3.23 (16) [4.63]
+// Small meshes run on 2 CTAs (the cheapest exchange), meshes from 512 cells
+// (WENO5: 256) on as many CTAs as divide them, up to 16.  MGP_MARCH_CS forces
+// the size, MGP_MARCH_MIN_SLAB the smallest slab, MGP_MARCH2=0 selects the
+// Field path.
 int march_cluster_size(const mgp_sweep_args &a) {
     // read per call (a getenv per launch), so tests can switch paths in-process
     const char *e = getenv("MGP_MARCH2");
     const int on = (e && atoi(e) == 0) ? 0 : 1;
-    int min_slab = env_int("MGP_MARCH_MIN_SLAB");
-    if (min_slab <= 0) min_slab = a.phi.weno_k == 0 ? 128 : 64;
+    const int min_slab_env = env_int("MGP_MARCH_MIN_SLAB");
     const int force = env_int("MGP_MARCH_CS");
     const int64_t nx = a.phi.nx;
     if (!on || a.n_chunks != 1 || a.tail != MGP_TAIL_NONE || a.phi.repeats != 1 || a.ref ||
@@ -2864,8 +2867,15 @@ int march_cluster_size(const mgp_sweep_args &a) {
         (a.g_mode == MGP_G_ARRAY && !a.g))
         return 0;
     int cs = force > 0 ? force : 16;
-    if (force <= 0)
-        while (cs > 2 && (nx % cs || nx / cs < min_slab)) cs /= 2;
+    if (force <= 0) {
+        if (min_slab_env > 0) {
+            while (cs > 2 && (nx % cs || nx / cs < min_slab_env)) cs /= 2;
+        } else if (nx >= (a.phi.weno_k == 2 ? 256 : 512)) {
+            while (cs > 2 && (nx % cs || nx / cs < 16)) cs /= 2;
+        } else {
+            cs = 2;
+        }
+    }
     if (cs != 2 && cs != 4 && cs != 8 && cs != 16) return 0;
     if (nx % cs || nx / cs < 8 || nx / cs > 256) return 0;
     return cs;

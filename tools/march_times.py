@@ -15,7 +15,7 @@ from paper_2104_09404_b200._lib import G_NONE, SUM_LANE2  # noqa: E402
 res = {}
 n = 512
 for order in (1, 3, 5):
-    for nx in (512, 1024, 4096):
+    for nx in (64, 128, 256, 512, 1024, 2048, 4096):
         op = P.SemiDiscreteOperator(P.make_model("burgers"), P.SpatialGrid(1.0, nx),
                                     P.FluxConfig("lf", P.WenoConfig(order)))
         phi = P.RungeKuttaStepper(op.rhs, 0.2 / nx, 3).phi_struct(SUM_LANE2)
