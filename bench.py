@@ -390,7 +390,9 @@ def run_ours(args):
     # ---- end to end through the public API with host buffers --------------
     # relax_to_host: C-points host->device, FCF relaxation, trajectory
     # device->host, the copies pipelined against the kernels (mgrit.py)
-    e2e_pieces = int(os.environ.get("MGP_E2E_PIECES", "0"))   # zero-copy: measured best (4 pieces -4 %)
+    # pieces of the pipelined relax_to_host: default = the API's own choice
+    # (zero-copy launch for small configs, 64 pipelined pieces at config 3)
+    e2e_pieces = int(os.environ["MGP_E2E_PIECES"]) if "MGP_E2E_PIECES" in os.environ else None
     e2e_graph = os.environ.get("MGP_E2E_GRAPH", "0") == "1"
     host_in = torch.empty(nc + 1, pb.n_x, dtype=torch.float64).pin_memory()
     host_in.copy_(serial[::pb.m, 0].cpu())
