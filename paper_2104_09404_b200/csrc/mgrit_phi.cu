@@ -212,7 +212,7 @@ constexpr int kModelBurgersRoe = 8;
 // address of the unrolled hot loops is the thread's base plus a literal),
 // one pad per 16 elements otherwise.  A half-warp's 64-bit accesses at
 // thread stride 2^LG + 1 words fall into 16 distinct bank pairs.
-__host__ __device__ constexpr int pad_log(int p) { return p == 8 ? 3 : (p == 4 ? 2 : 4); }   // 16 -> 4
+__host__ __device__ constexpr int pad_log(int p) { return p == 8 ? 3 : (p == 4 ? 2 : 4); }
 template <int LG>
 __host__ __device__ constexpr int skp(int t) { return t + (t >> LG); }
 template <int LG>
@@ -581,7 +581,7 @@ struct Field {
     }
     // thread-relative accessors (runs of 4 or 8 cells): element i0 + x with
     // x a literal after unrolling -> base register + immediate
-    static constexpr bool kRel = (P == 4 || P == 8 || P == 16);
+    static constexpr bool kRel = (P == 4 || P == 8);
     static constexpr bool kFusedCommit = true;   // phi_commit available (sweep_body)
     static constexpr bool kLL = LL && CS > 1;
     static __host__ __device__ constexpr int rel(int x) { return x + (x >> LG); }
@@ -3064,7 +3064,7 @@ struct FcfLaunch {
 
 template <int K, int P>
 int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
-    auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, (P == 16 ? 255 : MGP_REGS)>;
+    auto kern = fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>;
     const int ns = (int)phi.nx;
     L.nt = threads_for(ns, P);
     L.smem = smem_bytes(ns, K, 1, P);
@@ -3135,7 +3135,7 @@ int fcf_launch(const mgp_fcf_args &a, cudaStream_t st) {
         pl.R = 0;
         pl.W = pl.nchains + A;
     }
-    fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, (P == 16 ? 255 : MGP_REGS)>
+    fcf_kernel<K, MGP_SUM_SEQ, MGP_MODEL_BURGERS, P, MGP_REGS>
         <<<L.G, L.nt, L.smem, st>>>(a, make_consts(a.phi), pl);
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
@@ -3151,19 +3151,9 @@ bool fcf_supported(const mgp_phi &p, int64_t nc) {
            nc >= 1;
 }
 
-#ifdef MGP_P16   // experiment: runs of 16 cells, 256 threads for 4096 cells
-#define MGP_FCF_P16(KK)                                                 \
-        if (run == 16) return fn(std::integral_constant<int, KK>{},     \
-                                 std::integral_constant<int, 16>{});
-#else
-#define MGP_FCF_P16(KK)
-#endif
 template <class Fn>
 int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
-    int run = run_length(p.nx, nc > 1 ? nc : 2);
-#ifdef MGP_P16
-    if (p.nx >= 4096 && env_int("MGP_RUN") == 16) run = 16;
-#endif
+    const int run = run_length(p.nx, nc > 1 ? nc : 2);
     switch (p.weno_k) {
 #define MGP_FCF_K(KK)                                                   \
     case KK:                                                            \
@@ -3171,7 +3161,6 @@ int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
                                 std::integral_constant<int, 4>{});      \
         if (run == 8) return fn(std::integral_constant<int, KK>{},      \
                                 std::integral_constant<int, 8>{});      \
-        MGP_FCF_P16(KK)                                                 \
         return MGP_EINVAL;
 #ifndef MGP_QUICK
         MGP_FCF_K(0)
