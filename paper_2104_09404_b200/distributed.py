@@ -167,6 +167,39 @@ class DistMgritHierarchy:
         self._pristine = False
         return out
 
+    def relax_to_host(self, c_points_host: torch.Tensor, traj_host: torch.Tensor) -> None:
+        """This rank's ``relax_fine_values`` fed from and written back to
+        pinned host memory: the fused launch reads the local C-points
+        (n0 + 1 rows incl. the halo) from, and writes the local relaxed
+        trajectory (n0*m + 1 rows) to, the mapped pinned buffers itself
+        (MgritHierarchy._relax_to_host_direct); the boundary exchange and the
+        first interval's fix-up follow as in ``relax_fine_values``.  Falls
+        back to copy-in / relax / copy-out where the fused kernel does not
+        apply or the buffers are not pinned."""
+        m, nx, n0 = self.options.m, self.nx, self.nloc[0]
+        ws = self._fcf_workspace() if self.options.relaxation == "fcf" else None
+        th = traj_host.reshape(n0 * m + 1, nx)
+        if ws is None or not (c_points_host.is_pinned() and traj_host.is_pinned()):
+            self.load_c_points(c_points_host)
+            th.copy_(self.relax_fine_values(), non_blocking=True)
+            return
+        ch = c_points_host.reshape(n0 + 1, nx)
+        self.f_relax(0)
+        src = self._cur
+        d = self._other(src)
+        phi = self._phi(0, self._regime(0))
+        cd = self._c[d]
+        dev.relax_fcf(phi, n_chunks=n0, m=m, g_mode=G_ZERO, cs=ch, cd=cd, workspace=ws,
+                      fstore=th[1], f_cs=m * nx, f_ss=nx, cstore=th, cst_s=m * nx,
+                      f0_start=None if self.r == 0 else ch[0], what="relax_to_host")
+        self._send_right([cd[n0]], [cd[0]])
+        if self.r > 0:
+            th[0].copy_(cd[0], non_blocking=True)
+            dev.sweep(phi, n_chunks=1, start=cd[0], start_stride=0, n_steps=m - 1,
+                      g_mode=G_ZERO, store=th[1], st_ss=nx, what="relax_to_host/f0")
+        self._cur = self._fsrc = d
+        self._pristine = False
+
     def _other(self, i):
         if self._c[1 - i] is None:
             self._c[1 - i] = torch.empty_like(self._c[i])

@@ -74,6 +74,26 @@ def test_nccl_world1_relax_fine_values_is_the_fused_kernel(nccl_group):
                        g._c[g._cur])
 
 
+def test_nccl_world1_relax_to_host(nccl_group):
+    """The N > 1 bench's end-to-end step: one launch on mapped pinned buffers,
+    same rows as relax_fine_values."""
+    pb = P.Problem(name="d", n_x=128, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    st = pb.steppers(tg)
+    c = P.serial.march(st[0], u0, pb.n_t)[::4, 0]
+    h = DistMgritHierarchy(st, u0, tg, pb.space_grid(), pb.options())
+    g = DistMgritHierarchy(st, u0, tg, pb.space_grid(), pb.options())
+    c_host = c.cpu().pin_memory()
+    out = torch.empty(pb.n_t + 1, pb.n_x, dtype=torch.float64).pin_memory()
+    h.relax_to_host(c_host, out)
+    torch.cuda.synchronize()
+    g.load_c_points(c)
+    want = g.relax_fine_values()
+    assert torch.equal(out, want.reshape(out.shape).cpu())
+    assert torch.equal(h._c[h._cur], g._c[g._cur])
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

@@ -213,6 +213,28 @@ def test_relax_to_host_equals_relax_then_fine_values(relaxation, pieces):
     assert torch.equal(h.fine_values().cpu(), out)
 
 
+@pytest.mark.parametrize("n_t,kind", [(256, "one zero-copy launch"), (16384, "16 pipelined pieces")])
+def test_relax_to_host_default_choice(n_t, kind):
+    """pieces=None: below 4096 CF-intervals one launch on the mapped pinned
+    buffers, from 4096 on pipelined pieces of 256 intervals; either way the
+    result of relax(0) + fine_values()."""
+    pb = P.Problem(name="io", n_x=64, n_t=n_t, cfl=0.2, n_modes=3, n_levels=2, m=4)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    serial = P.serial.march(steppers[0], u0, pb.n_t)
+    c_host = serial[::4, 0].cpu().pin_memory()
+    out = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64).pin_memory()
+    h = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    h.relax_to_host(c_host, out)
+    torch.cuda.synchronize()
+    g = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+    g.load_c_points(c_host)
+    g.relax(0)
+    assert torch.equal(out, g.fine_values().cpu()), kind
+    assert torch.equal(h.fine_values().cpu(), out), kind
+
+
 def test_relax_to_host_graph_replay():
     pb = P.Problem(name="io", n_x=64, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4)
     u0 = pb.initial_state()
