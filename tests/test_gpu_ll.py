@@ -66,7 +66,9 @@ def _both(fn):
 
 
 @pytest.mark.parametrize("nx,nc", [(8192, 3), (8192, 90), (16384, 5), (32768, 4),
-                                   (65536, 2), (65536, 20)])
+                                   (65536, 2), (65536, 20),
+                                   (8200, 5),      # 4 slabs of 2050 cells: partial last run
+                                   (12300, 3)])    # 4 slabs of 3075 cells (odd)
 @pytest.mark.parametrize("g_mode", [G_ZERO, G_ARRAY])
 def test_chained_steps_and_tail_phi(nx, nc, g_mode):
     st = _stepper(nx)
@@ -88,7 +90,7 @@ def test_chained_steps_and_tail_phi(nx, nc, g_mode):
     assert torch.equal(s1, s0) and torch.equal(t1, t0)
 
 
-@pytest.mark.parametrize("nx,nc", [(8192, 4), (16384, 3)])
+@pytest.mark.parametrize("nx,nc", [(8192, 4), (16384, 3), (8200, 3), (12300, 2)])
 def test_against_oracle(nx, nc):
     st = _stepper(nx)
     x = _fields(nx, nc, 11)
