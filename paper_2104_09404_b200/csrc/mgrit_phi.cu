@@ -192,14 +192,14 @@ constexpr int kModelBurgersRoe = 8;
 #endif
 // Unroll factor of the centred reconstruction: half a run per block (two
 // blocks of 4 windows for runs of 8 cells, of 2 for runs of 4).  Measured on
-// B200 (profiles/r02_fcf_unroll.txt): C3 16.3 -> 17.8 G point-updates/s --
+// B200 (profiles/r02_fcf_unroll.txt; runs of 16: blocks of 4): C3 16.3 -> 17.8 G point-updates/s --
 // the 8-window block spilled 824 bytes at 128 registers, the 4-window block
 // none inside the loop, and its static schedule has 19 % fewer stall cycles
 // per window; C2 (runs of 4) 14.2 -> 14.6 G.  MGP_CENTRED_UNROLL overrides.
 #ifdef MGP_CENTRED_UNROLL
 #define MGP_CU(pc) MGP_CENTRED_UNROLL
 #else
-#define MGP_CU(pc) ((pc) >= 4 ? (pc) / 2 : (pc))
+#define MGP_CU(pc) ((pc) >= 8 ? 4 : ((pc) >= 4 ? (pc) / 2 : (pc)))
 #endif
 #define MGP_PRAGMA(x) _Pragma(#x)
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
@@ -523,8 +523,30 @@ __device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned 
 // CTA's halo through distributed shared memory when committed), the states of
 // the interface just left of the slab are pushed by the left neighbour, and
 // alpha is reduced over the cluster.
-template <int K, int REG, int MODEL, int P, int CS, bool LL = false>
+// 256-bit global accesses (sm_100): a thread's slice of its CTA's RK-base row
+__device__ __forceinline__ void ldg_cg4(const double *p, double *v) {
+    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void stg_cg4(double *p, const double *v) {
+    asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                 "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
+// U0G: the Runge-Kutta base state lives in a global scratch row of the CTA
+// (L2-resident, each thread reads and writes only its own run) instead of a
+// fourth shared-memory array: a 4096-cell field then needs 105 KB and two
+// CTAs fit one SM (256 threads x runs of 16 cells x 128 registers each).
+// Measured: equal work on smaller meshes runs 0.84-0.88 of the FP64 peak with
+// 2-4 CTAs per SM against 0.77 with one (profiles/r02_fcf_u0g.txt) -- one
+// CTA's stage tails and barriers hide behind the other's reconstruction.
+// Only full runs, only the fused-commit propagator (phi_commit).
+template <int K, int REG, int MODEL, int P, int CS, bool LL = false, bool U0G = false>
 struct Field {
+    double *u0g;              // U0G: this CTA's RK-base row (global)
     // LL: the CS CTAs exchange through the global mailbox `mbox` (this
     // group's region) instead of distributed shared memory
     unsigned long long *mbox;
@@ -566,7 +588,7 @@ struct Field {
         o_L = o_u + sk_size(ns + 2 * H);
         o_R = o_L + sk_size(ns);
         o_u0 = o_R + sk_size(ns);
-        return o_u0 + sk_size(ns);
+        return U0G ? o_u0 : o_u0 + sk_size(ns);
     }
     __device__ __forceinline__ double &s_u(int idx) const { return mgp_sm[o_u + idx]; }
     __device__ __forceinline__ double &s_L(int idx) const { return mgp_sm[o_L + idx]; }
@@ -581,7 +603,7 @@ struct Field {
     }
     // thread-relative accessors (runs of 4 or 8 cells): element i0 + x with
     // x a literal after unrolling -> base register + immediate
-    static constexpr bool kRel = (P == 4 || P == 8);
+    static constexpr bool kRel = (P == 4 || P == 8 || P == 16);
     static constexpr bool kFusedCommit = true;   // phi_commit available (sweep_body)
     static constexpr bool kLL = LL && CS > 1;
     static __host__ __device__ constexpr int rel(int x) { return x + (x >> LG); }
@@ -1011,10 +1033,18 @@ struct Field {
         return (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
     }
 
-    __device__ __forceinline__ void rhs(const Consts &k, double *A) {
+    __device__ __forceinline__ void rhs(const Consts &k, double *A, double *u0r = nullptr,
+                                        int sg = 0) {
         trace(1);
         unsigned long long m = reconstruct(k);
         trace(2);
+        if (U0G && sg > 0) {
+            // the RK base of the run, issued ahead of the alpha barrier that
+            // hides its L2 latency (a thread beyond the field reads its own
+            // padding slice of the row)
+#pragma unroll
+            for (int p = 0; p < (U0G ? PC : 0); p += 4) ldg_cg4(u0g + i0 + p, u0r + p);
+        }
         double half_alpha;
         if (MODEL == MGP_MODEL_BURGERS) {
             m = warp_umax64(m);
@@ -1144,7 +1174,8 @@ struct Field {
     // selected once, outside the cell loop.
     // FULL: a full run addressed by literal offsets (no per-cell range test)
     template <bool FULL>
-    __device__ __forceinline__ double u0v(int p) const {
+    __device__ __forceinline__ double u0v(int p, const double *u0r) const {
+        if (U0G) return u0r[p];
         if (FULL) return u0_rel(p);
         return u0(p);
     }
@@ -1155,7 +1186,7 @@ struct Field {
     }
     template <bool FULL = false>
     __device__ __forceinline__ void rk_update(const Consts &k, int rk, int sg, const double *A,
-                                              double *st) {
+                                              double *st, const double *u0r) {
         const int code = rk == 0 ? 0 : (sg == 0 ? 1 : (rk == 2 ? 2 : (sg == 1 ? 3 : 4)));
         switch (code) {
             case 0:
@@ -1164,17 +1195,17 @@ struct Field {
                 break;
             case 1:
 #pragma unroll
-                for (int p = 0; p < PC; ++p) st[p] = u0v<FULL>(p) + k.dt * A[p];
+                for (int p = 0; p < PC; ++p) st[p] = u0v<FULL>(p, u0r) + k.dt * A[p];
                 break;
             case 2:
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
-                    st[p] = ((0.5 * u0v<FULL>(p)) + (0.5 * stv<FULL>(p))) + (k.hdt * A[p]);
+                    st[p] = ((0.5 * u0v<FULL>(p, u0r)) + (0.5 * stv<FULL>(p))) + (k.hdt * A[p]);
                 break;
             case 3:
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
-                    st[p] = ((0.75 * u0v<FULL>(p)) + (0.25 * stv<FULL>(p))) + (k.qdt * A[p]);
+                    st[p] = ((0.75 * u0v<FULL>(p, u0r)) + (0.25 * stv<FULL>(p))) + (k.qdt * A[p]);
                 break;
             default: {
                 // u0 / 3.0: the reciprocal of 3 refined once for the run
@@ -1184,10 +1215,10 @@ struct Field {
                 bool bad = false;
                 double third[PC];
 #pragma unroll
-                for (int p = 0; p < PC; ++p) third[p] = mgp::div_fast(u0v<FULL>(p), R3, bad);
+                for (int p = 0; p < PC; ++p) third[p] = mgp::div_fast(u0v<FULL>(p, u0r), R3, bad);
                 if (bad) {
 #pragma unroll 1
-                    for (int p = 0; p < PC; ++p) third[p] = mgp::div_slow(u0v<FULL>(p), 3.0);
+                    for (int p = 0; p < PC; ++p) third[p] = mgp::div_slow(u0v<FULL>(p, u0r), 3.0);
                 }
 #pragma unroll
                 for (int p = 0; p < PC; ++p)
@@ -1202,12 +1233,16 @@ struct Field {
     // result slots (result(t)).
     template <bool FUSED>
     __device__ __forceinline__ void phi_t(const Consts &k, int rk, int g_mode) {
+        static_assert(!U0G || (FUSED && (P % 4 == 0) && CS == 1),
+                      "U0G: fused commit, full runs of a multiple of 4 cells, one CTA per field");
+        if (!U0G) {
 #pragma unroll
-        for (int p = 0; p < PC; ++p)
-            if (i0 + p < ns) {
-                if (kRel) u0_rel(p) = u_rel(p);
-                else s_u0(sk(i0 + p)) = cell(i0 + p);
-            }
+            for (int p = 0; p < PC; ++p)
+                if (i0 + p < ns) {
+                    if (kRel) u0_rel(p) = u_rel(p);
+                    else s_u0(sk(i0 + p)) = cell(i0 + p);
+                }
+        }
         const int stages = rk == 0 ? 1 : rk;
         // one call site of the reconstruction for every stage (code size)
 #pragma unroll 1
@@ -1217,13 +1252,29 @@ struct Field {
                 sync();  // committed stage values (and halos) visible
             }
             double A[PC];
-            rhs(k, A);
+            double u0r[U0G ? PC : 1];
+            rhs(k, A, u0r, sg);
             double st[PC];
-            if (kMerged && kRel && i0 + PC <= ns) rk_update<true>(k, rk, sg, A, st);
-            else rk_update<false>(k, rk, sg, A, st);
+            if (U0G) {
+                if (sg == 0) {
+                    // the stage input is the RK base: keep it for the later
+                    // stages (this thread's slice of the CTA's global row)
+#pragma unroll
+                    for (int p = 0; p < (U0G ? PC : 0); ++p) u0r[p] = u_rel(p);
+                    if (stages > 1) {
+#pragma unroll
+                        for (int p = 0; p < (U0G ? PC : 0); p += 4) stg_cg4(u0g + i0 + p, u0r + p);
+                    }
+                }
+                rk_update<true>(k, rk, sg, A, st, u0r);
+            } else if (kMerged && kRel && i0 + PC <= ns) {
+                rk_update<true>(k, rk, sg, A, st, u0r);
+            } else {
+                rk_update<false>(k, rk, sg, A, st, u0r);
+            }
             if (sg < stages - 1) {
                 commit(st);
-            } else if (FUSED) {
+            } else if constexpr (FUSED) {
                 if (g_mode == MGP_G_ZERO) {
 #pragma unroll
                     for (int p = 0; p < PC; ++p) st[p] = st[p] + 0.0;
@@ -1865,6 +1916,7 @@ struct FcfPlan {
     bool fstore;
     int ordered;              // > 0: chain starts read C-points from host memory (zero-copy);
                               // keep at most `ordered` rows in flight, in ticket order
+    int64_t u0_off;           // U0G kernels: byte offset of the CTAs' RK-base rows in the workspace
     __host__ __device__ int len(int64_t j) const {
         if (!fstore) return m;
         if (j < nc - 1) return L;
@@ -1933,8 +1985,14 @@ template <int K, int REG, int MODEL, int P, int REGS>
 __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts k,
                                              const FcfPlan pl) {
     __shared__ long long s_ticket, s_chain;
-    using F = Field<K, REG, MODEL, P, 1>;
+    constexpr bool kU0G = (P == 16);   // runs of 16: two CTAs per SM for 4096-cell fields
+    using F = Field<K, REG, MODEL, P, 1, false, kU0G>;
     F f;
+    // one row of blockDim.x runs per CTA (threads beyond the field, where the
+    // block size is rounded up to a warp, own padding slices)
+    f.u0g = kU0G ? reinterpret_cast<double *>(static_cast<char *>(a.workspace) + pl.u0_off) +
+                       (size_t)blockIdx.x * (size_t)blockDim.x * P
+                 : nullptr;
     const int ns = (int)a.phi.nx;
     const int tid = threadIdx.x, nt = blockDim.x;
     f.q = 0;
@@ -2706,7 +2764,9 @@ size_t smem_bytes(int64_t ns, int k, int cs, int p) {
     const auto size = [p](int n) {   // Field::sk_size for run length p
         return p == 8 ? skp_size<3>(n) : (p == 4 ? skp_size<2>(n) : skp_size<4>(n));
     };
-    return sizeof(double) * (size_t)(size((int)ns + 2 * H) + 3 * size((int)ns) + 3 * 32 +
+    // runs of 16 (fcf_kernel, Field U0G): no RK-base array
+    const int arrays = p == 16 ? 2 : 3;
+    return sizeof(double) * (size_t)(size((int)ns + 2 * H) + arrays * size((int)ns) + 3 * 32 +
                                      3 * cs + 2) +
            sizeof(unsigned long long) * (size_t)(cs + 32);
 }
@@ -3059,7 +3119,7 @@ int launch_sys(const mgp_sweep_args &a, cudaStream_t st) {
 struct FcfLaunch {
     int G = 0, nt = 0;
     size_t smem = 0;
-    int64_t R = 0, Gmax = 0, bytes = 0;
+    int64_t R = 0, Gmax = 0, bytes = 0, u0_off = 0;
 };
 
 template <int K, int P>
@@ -3085,6 +3145,11 @@ int fcf_setup(const mgp_phi &phi, int64_t nc, bool fstore, FcfLaunch &L) {
     L.G = (int)G;
     L.R = nchains > G ? G : 0;
     L.bytes = (4 + L.Gmax) * 8 + L.Gmax * ns * (int64_t)sizeof(double);
+    L.u0_off = 0;
+    if (P == 16) {   // U0G: one RK-base row per resident CTA, 256-byte aligned
+        L.u0_off = (L.bytes + 255) / 256 * 256;
+        L.bytes = L.u0_off + L.Gmax * (int64_t)L.nt * P * (int64_t)sizeof(double);
+    }
     return MGP_OK;
 }
 
@@ -3103,6 +3168,7 @@ int fcf_launch(const mgp_fcf_args &a, cudaStream_t st) {
     pl.L = fstore ? 2 * a.m - 1 : a.m;
     pl.R = L.R;
     pl.Gmax = L.Gmax;
+    pl.u0_off = L.u0_off;
     pl.K = pl.nchains - L.R;
     // segment length of the chains taken last; measured on B200 for C2
     // shapes: whole chains (S = L) and S = 1, 2 within 1-2 %
@@ -3153,7 +3219,14 @@ bool fcf_supported(const mgp_phi &p, int64_t nc) {
 
 template <class Fn>
 int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
-    const int run = run_length(p.nx, nc > 1 ? nc : 2);
+    int run = run_length(p.nx, nc > 1 ? nc : 2);
+    // WENO5 fields above 2048 cells (one CTA per SM with four shared arrays):
+    // runs of 16 cells with the RK base in global memory, two CTAs per SM
+    // (Field U0G).  MGP_FCF_U0G=0 keeps the runs of 8.
+    if (p.weno_k == 2 && p.nx > 2048 && p.nx % 16 == 0) {
+        const char *e = getenv("MGP_FCF_U0G");
+        if (!(e && atoi(e) == 0)) run = 16;
+    }
     switch (p.weno_k) {
 #define MGP_FCF_K(KK)                                                   \
     case KK:                                                            \
@@ -3161,6 +3234,11 @@ int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
                                 std::integral_constant<int, 4>{});      \
         if (run == 8) return fn(std::integral_constant<int, KK>{},      \
                                 std::integral_constant<int, 8>{});      \
+        if (run == 16) {                                                \
+            if constexpr (KK == 2)                                      \
+                return fn(std::integral_constant<int, KK>{},            \
+                          std::integral_constant<int, 16>{});           \
+        }                                                               \
         return MGP_EINVAL;
 #ifndef MGP_QUICK
         MGP_FCF_K(0)

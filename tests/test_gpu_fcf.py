@@ -42,6 +42,10 @@ CASES = [
     (128, 1024, 4, 1, "fe"),          # first order
     (128, 1024, 4, 7, "ssprk3"),      # WENO7
     (1024, 2048, 4, 5, "ssprk3"),     # runs of 8 cells per thread
+    (4096, 2400, 4, 5, "ssprk3"),     # runs of 16, RK base in global memory, 2 CTAs/SM;
+                                      # 600 intervals > 296 CTA slots
+    (2064, 256, 4, 5, "ssprk2"),      # runs of 16, 129 threads' worth of cells, SSP-RK2
+    (3000, 64, 2, 5, "ssprk3"),       # above 2048 but not a multiple of 16: runs of 8
 ]
 
 
