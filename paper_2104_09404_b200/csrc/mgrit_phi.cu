@@ -1233,8 +1233,8 @@ struct Field {
     // result slots (result(t)).
     template <bool FUSED>
     __device__ __forceinline__ void phi_t(const Consts &k, int rk, int g_mode) {
-        static_assert(!U0G || (FUSED && (P % 4 == 0) && CS == 1),
-                      "U0G: fused commit, full runs of a multiple of 4 cells, one CTA per field");
+        static_assert(!U0G || (FUSED && (P % 4 == 0) && (CS == 1 || LL)),
+                      "U0G: fused commit, full runs of a multiple of 4 cells, no hardware cluster");
         if (!U0G) {
 #pragma unroll
             for (int p = 0; p < PC; ++p)
@@ -1376,12 +1376,14 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
             }
         }
-        // Plain chained steps without a g array: the last stage commits its
-        // state (+ 0.0 per g_mode) straight into s_u (Field::phi_commit);
-        // after the barrier that publishes it, the step's store / error /
-        // non-finite count read it back from s_u in coalesced order while
-        // the next step's reconstruction starts.
-        const bool fused = F::kFusedCommit && a.g_mode != MGP_G_ARRAY && a.phi.repeats == 1;
+        // WENO/RK fields (Field): every propagator application commits its
+        // last stage straight into s_u (Field::phi_commit) -- the next step's
+        // input, and where every epilogue reads the result (cell(t)) after
+        // the barrier that publishes it.  Plain chained steps without a g
+        // array add their + 0.0 in the commit and leave the step's store /
+        // error / non-finite count pending: they read s_u back in coalesced
+        // order while the next step's reconstruction starts.
+        const bool fused = F::kFusedCommit && a.g_mode != MGP_G_ARRAY;
         bool pending = false;
         double *p_st = nullptr;
         const double *p_rs = nullptr;
@@ -1405,26 +1407,50 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
             f.sync();  // s_u and halos complete
             if (pending) flush();
             if constexpr (F::kFusedCommit) {
-                if (fused && s <= a.n_steps) {
-                    f.phi_commit(k, rk, a.g_mode);
+                const bool step = s <= a.n_steps;
+                // ComposedStepper (stepper.py:170-188): Phi = inner^repeats
+#pragma unroll 1
+                for (int rep = a.phi.repeats; rep > 0; --rep) {
+                    f.phi_commit(k, rk, (rep == 1 && step && fused) ? a.g_mode : MGP_G_NONE);
+                    if (rep > 1) f.sync();
+                }
+                if (step && fused) {
                     p_st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
                     p_rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
                     pending = true;
                     continue;
                 }
-            }
+                f.sync();   // the committed result (and its halos) visible
+                if (step) {
+                    // + g in place: each thread updates the cells it reads
+                    f.begin_halo_exchange();
+                    const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
+                    double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
+                    const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
+                    for (int t = tid; t < ns; t += nt) {
+                        const int c = c0 + t;
+                        const double v = add_g(f.cell(t), a.g_mode, g, c);
+                        f.put(t, v);
+                        if (st) st[c] = v;
+                        if (rs) {
+                            const double d = v - rs[c];
+                            acc_e = acc_e + d * d;
+                        }
+                        if (a.count_nonfinite && !is_finite(v)) acc_n += 1.0;
+                    }
+                    continue;
+                }
+            } else {
             f.phi(k, rk);
             __syncthreads();   // results complete
             // ComposedStepper (stepper.py:170-188): Phi = inner^repeats
             for (int rep = 1; rep < a.phi.repeats; ++rep) {
-                if constexpr (F::kFusedCommit) f.begin_halo_exchange();
                 for (int t = tid; t < ns; t += nt) f.put(t, f.result(t));
                 f.sync();
                 f.phi(k, rk);
                 __syncthreads();
             }
             if (s <= a.n_steps) {
-                if constexpr (F::kFusedCommit) f.begin_halo_exchange();
                 const double *g = a.g ? a.g + b * a.g_cs + (int64_t)(s - 1) * a.g_ss : nullptr;
                 double *st = a.store ? a.store + b * a.st_cs + (int64_t)(s - 1) * a.st_ss : nullptr;
                 const double *rs = ref ? ref + (int64_t)s * a.ref_ss : nullptr;
@@ -1441,11 +1467,18 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 }
                 continue;
             }
+            }   // propagators with result slots (one-step LF family, systems)
+            // the tail's Phi(x): Field committed it into s_u, the others hold
+            // it in their result slots
+            auto res = [&](int t) {
+                if constexpr (F::kFusedCommit) return f.cell(t);
+                else return f.result(t);
+            };
             const double *tg = a.tail_g ? a.tail_g + b * a.tg_s : nullptr;
             if (a.tail == MGP_TAIL_PHI) {
                 double *out = a.tail_out + b * a.to_s;
                 for (int t = tid; t < ns; t += nt)
-                    out[c0 + t] = add_g(f.result(t), a.tail_g_mode, tg, c0 + t);
+                    out[c0 + t] = add_g(res(t), a.tail_g_mode, tg, c0 + t);
             } else if (a.tail == MGP_TAIL_RESTRICT) {
                 // mgrit.py:211-215: g_c = (g_f + phi) - psi;
                 // u_c = phi + g_f (last-step) or u_f (injection)
@@ -1458,7 +1491,7 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                     const double p = phi[c];
                     const double left =
                         (a.tail_g_mode == MGP_G_NONE) ? p : g_value(a.tail_g_mode, tg, c) + p;
-                    gc[c] = left - f.result(t);
+                    gc[c] = left - res(t);
                     uc[c] = (a.guess == MGP_GUESS_LAST_STEP) ? add_g(p, a.tail_g_mode, tg, c)
                                                              : uf[c];
                 }
@@ -1468,7 +1501,7 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 const double *rn = (last && a.ref) ? a.ref + (b + 1) * a.ref_cs : nullptr;
                 for (int t = tid; t < ns; t += nt) {
                     const int c = c0 + t;
-                    const double y = f.result(t);
+                    const double y = res(t);
                     const double pred =
                         (a.tail_g_mode == MGP_G_NONE) ? y : g_value(a.tail_g_mode, tg, c) + y;
                     const double u = tgt[c];
@@ -1552,9 +1585,13 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
 
 template <int K, int REG, int MODEL, int P, int REGS, int CS, bool LL = false>
 __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k,
-                                               unsigned long long *mbox) {
-    using F = Field<K, REG, MODEL, P, CS, LL>;
+                                               unsigned long long *mbox, double *u0_rows) {
+    // runs of 16 cells: the RK base in a global row per CTA (Field U0G), so
+    // that two CTAs of a 4096-cell field or slab share an SM
+    constexpr bool kU0G = (P == 16);
+    using F = Field<K, REG, MODEL, P, CS, LL, kU0G>;
     F f;
+    f.u0g = kU0G ? u0_rows + (size_t)blockIdx.x * (size_t)blockDim.x * (P > 0 ? P : 1) : nullptr;
     f.eA = f.eB = f.eC = 0;
     f.halo_pending = false;
     // LL: this group's region of the mailbox (zeroed by the launch)
@@ -2771,34 +2808,39 @@ size_t smem_bytes(int64_t ns, int k, int cs, int p) {
            sizeof(unsigned long long) * (size_t)(cs + 32);
 }
 
-// LL mailbox (Field, LL mode): one allocation per device and stream, grown on
-// demand, zeroed by every launch that uses it (tags restart at 1).
-unsigned long long *ll_mailbox(size_t words, cudaStream_t st) {
+// Library-owned device scratch, one allocation per (kind, device, stream),
+// grown on demand: kind 0 = the LL mailbox (Field, LL mode; zeroed by every
+// launch that uses it, tags restart at 1), kind 1 = the RK-base rows of the
+// runs-of-16 sweep kernels (Field U0G; no initialisation needed).
+void *device_scratch(int kind, size_t bytes, cudaStream_t st, bool zero) {
     struct Box {
-        int dev;
+        int kind, dev;
         cudaStream_t st;
-        unsigned long long *p;
-        size_t words;
+        void *p;
+        size_t bytes;
     };
     static std::vector<Box> boxes;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     Box *bx = nullptr;
     for (auto &b : boxes)
-        if (b.dev == dev && b.st == st) bx = &b;
+        if (b.kind == kind && b.dev == dev && b.st == st) bx = &b;
     if (!bx) {
-        boxes.push_back(Box{dev, st, nullptr, 0});
+        boxes.push_back(Box{kind, dev, st, nullptr, 0});
         bx = &boxes.back();
     }
-    if (bx->words < words) {
-        if (bx->p) cudaFree(bx->p);
+    if (bx->bytes < bytes) {
+        if (bx->p) {
+            // work of earlier launches on this stream may still use the old block
+            if (cudaStreamSynchronize(st) != cudaSuccess) return nullptr;
+            cudaFree(bx->p);
+        }
         bx->p = nullptr;
-        bx->words = 0;
-        if (cudaMalloc(&bx->p, words * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
-        bx->words = words;
+        bx->bytes = 0;
+        if (cudaMalloc(&bx->p, bytes) != cudaSuccess) return nullptr;
+        bx->bytes = bytes;
     }
-    if (cudaMemsetAsync(bx->p, 0, words * sizeof(unsigned long long), st) != cudaSuccess)
-        return nullptr;
+    if (zero && cudaMemsetAsync(bx->p, 0, bytes, st) != cudaSuccess) return nullptr;
     return bx->p;
 }
 
@@ -2814,20 +2856,30 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     if (grid > ((int64_t)1 << 30) / CS) grid = ((int64_t)1 << 30) / CS;
     const Consts k = make_consts(a.phi);
     unsigned long long *mbox = nullptr;
-    if (CS == 1) {
-        kern<<<(unsigned)grid, nt, sm, st>>>(a, k, mbox);
-    } else if (LL) {
-        // groups of CS co-resident CTAs (cooperative launch: all resident or
-        // the launch fails), as many groups as fit the device
-        int dev = 0, nsm = 0, per = 0;
+    double *u0_rows = nullptr;
+    int dev = 0, nsm = 0, per = 0;
+    if (P == 16 || LL) {
         if (cudaGetDevice(&dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm) != cudaSuccess)
             return MGP_ECUDA;
+        // one field (group) per resident slot; the kernel strides over the chunks
         const int64_t groups = (int64_t)per * nsm / CS;
         if (groups < 1) return MGP_ECUDA;
         if (grid > groups) grid = groups;
-        mbox = ll_mailbox((size_t)grid * 2 * CS * kLLWords, st);
+    }
+    if (P == 16) {
+        u0_rows = static_cast<double *>(
+            device_scratch(1, (size_t)grid * CS * nt * 16 * sizeof(double), st, false));
+        if (!u0_rows) return MGP_ECUDA;
+    }
+    if (CS == 1) {
+        kern<<<(unsigned)grid, nt, sm, st>>>(a, k, mbox, u0_rows);
+    } else if (LL) {
+        // groups of CS co-resident CTAs (cooperative launch: all resident or
+        // the launch fails), as many groups as fit the device
+        mbox = static_cast<unsigned long long *>(device_scratch(
+            0, (size_t)grid * 2 * CS * kLLWords * sizeof(unsigned long long), st, true));
         if (!mbox) return MGP_ECUDA;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid * CS));
@@ -2839,7 +2891,7 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox, u0_rows) != cudaSuccess) return MGP_ECUDA;
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid * CS));
@@ -2853,7 +2905,7 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox, u0_rows) != cudaSuccess) return MGP_ECUDA;
     }
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
@@ -2958,6 +3010,10 @@ int launch_r(const mgp_sweep_args &a, cudaStream_t st) {
     return launch_t<K, REG, MODEL, P, MGP_REGS, 1>(a, st);
 }
 
+// The runs-of-16 / RK-base-in-global variant (Field U0G, two CTAs per SM for
+// 4096-cell fields) pays for the fused FCF launch only: the batched sweeps
+// measured slower with it (C3 F+C sweep 20.2 -> 19.7 G point-updates/s, C5 LL
+// sweep 15.8 -> 15.3; profiles/r02_fcf_u0g.txt), so they keep runs of 8.
 template <int K, int REG, int MODEL>
 int launch_p(const mgp_sweep_args &a, cudaStream_t st) {
     const int cs = cluster_size(a);
