@@ -675,9 +675,10 @@ struct Field {
     static constexpr int HALO = H;
     __device__ __forceinline__ double cell(int t) const { return s_u(sk(t + H)); }
     __device__ __forceinline__ void load(int t, double v) { s_u(sk(t + H)) = v; }
-    // centred reconstruction with the merged flux / rhs pass: the interface
-    // states stay readable by neighbouring runs until the stage ends, so
-    // results go to the RK base slots, which only their owner reads.  On a
+    // centred reconstruction with the merged flux / rhs pass: each thread
+    // forms the flux of the interface left of its run itself; the stage
+    // values are committed into s_u after the alpha barrier, when every
+    // reconstruction has read it.  On a
     // cluster (CS > 1) the slab's last window (centred on the right
     // neighbour's cell 0) is the neighbour's left state of its interface 0,
     // pushed into its s_L; the states of the interface left of the slab
@@ -688,9 +689,6 @@ struct Field {
 #else
         P > 0 && K > 0;
 #endif
-    __device__ __forceinline__ double result(int t) const {
-        return kMerged ? s_u0(sk(t)) : s_R(sk(t));
-    }
     __device__ __forceinline__ void put(int t, double v) {
         s_u(sk(t + H)) = v;
         if (CS == 1) {
@@ -1160,11 +1158,9 @@ struct Field {
         trace(4);
     }
 
-    // res = RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned
-    // cells, written to s_R[sk(c)]; rk_order 0 gives the rhs.  Precondition:
-    // s_u complete and synchronised.  Leaves s_u holding the last stage input.
-    // The RK base and the stage values live in shared memory (s_u0, s_u), so
-    // no per-cell state is held in registers across the reconstruction.
+    // The RK base and the stage values live in shared memory (s_u0, s_u; the
+    // base in a global row with U0G), so no per-cell state is held in
+    // registers across the reconstruction.
     __device__ __forceinline__ double u0(int p) const {
         return (i0 + p < ns) ? (kRel ? u0_rel(p) : s_u0(sk(i0 + p))) : 0.0;
     }
@@ -1227,14 +1223,15 @@ struct Field {
         }
     }
 
-    // FUSED: the last stage's values (+ g, sweep_body's add_g for the modes
-    // without an array) are committed straight into s_u with their halo
-    // copies, ready to be the next step's input; otherwise they go to the
-    // result slots (result(t)).
-    template <bool FUSED>
-    __device__ __forceinline__ void phi_t(const Consts &k, int rk, int g_mode) {
-        static_assert(!U0G || (FUSED && (P % 4 == 0) && (CS == 1 || LL)),
-                      "U0G: fused commit, full runs of a multiple of 4 cells, no hardware cluster");
+    // Phi = RungeKuttaStepper.advance(s_u) (stepper.py:50-62) for the owned
+    // cells; rk_order 0 gives the rhs.  The last stage's values (+ 0.0 for
+    // g_mode ZERO, sweep_body's add_g for the modes without an array) are
+    // committed straight into s_u with their halo copies: the next step's
+    // input, and where every epilogue reads the result (cell(t)) after the
+    // barrier that publishes it.
+    __device__ __forceinline__ void phi_commit(const Consts &k, int rk, int g_mode) {
+        static_assert(!U0G || ((P % 4 == 0) && (CS == 1 || LL)),
+                      "U0G: full runs of a multiple of 4 cells, no hardware cluster");
         if (!U0G) {
 #pragma unroll
             for (int p = 0; p < PC; ++p)
@@ -1272,24 +1269,12 @@ struct Field {
             } else {
                 rk_update<false>(k, rk, sg, A, st, u0r);
             }
-            if (sg < stages - 1) {
-                commit(st);
-            } else if constexpr (FUSED) {
-                if (g_mode == MGP_G_ZERO) {
+            if (sg == stages - 1 && g_mode == MGP_G_ZERO) {
 #pragma unroll
-                    for (int p = 0; p < PC; ++p) st[p] = st[p] + 0.0;
-                }
-                commit(st);
-            } else {
-                store_res(st);
+                for (int p = 0; p < PC; ++p) st[p] = st[p] + 0.0;
             }
+            commit(st);
         }
-    }
-    __device__ __forceinline__ void phi(const Consts &k, int rk) {
-        phi_t<false>(k, rk, MGP_G_NONE);
-    }
-    __device__ __forceinline__ void phi_commit(const Consts &k, int rk, int g_mode) {
-        phi_t<true>(k, rk, g_mode);
     }
 
     __device__ __forceinline__ double stage(int p) const {
@@ -1325,14 +1310,6 @@ struct Field {
 #pragma unroll
         for (int p = 0; p < PC; ++p)
             if (i0 + p < ns) put(i0 + p, v[p]);
-    }
-    __device__ __forceinline__ void store_res(const double *v) {
-#pragma unroll
-        for (int p = 0; p < PC; ++p)
-            if (i0 + p < ns) {
-                if (kRel) (kMerged ? u0_rel(p) : R_rel(p)) = v[p];
-                else (kMerged ? s_u0(sk(i0 + p)) : s_R(sk(i0 + p))) = v[p];
-            }
     }
 };
 
