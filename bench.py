@@ -497,6 +497,8 @@ def run_ours(args):
         "kernel_ms": ({"fcf": statistics.median(k_fc)} if fused else
                       {"fused_f_c": statistics.median(k_fc), "f_store": statistics.median(k_f)}),
     }
+    if world == 1 and not force_dist and args.workload != "c2":
+        line["config2"] = side_workload("c2", flush, stream)   # round 1's bench workload, for context
     if not args.no_cpu_baseline and world == 1:
         rate, cores, n, el = cpu_relax_rate(pb, args.cpu_seconds)
         nci = min(CPU_SAMPLE_INTERVALS, nc)
@@ -507,6 +509,52 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def side_workload(name, flush, stream, steps=20):
+    """The same step and iteration on another BASELINE config (device-timed
+    only), reported as extra keys next to the headline workload."""
+    import torch
+
+    import paper_2104_09404_b200 as P
+    pb = workload(name)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    sg = pb.space_grid()
+    steppers = pb.steppers(tg)
+    serial = P.serial.march(steppers[0], u0, pb.n_t)
+    h = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+    h.load_c_points(serial[::pb.m, 0])
+    traj = torch.empty(pb.n_t + 1, 1, pb.n_x, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        h.relax_fine_values(out=traj)
+    ev = []
+    for _ in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h.relax_fine_values(out=traj)
+        b.record(stream)
+        ev.append((a, b))
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    it = []
+    for i in range(4):
+        hi = P.MgritHierarchy(steppers, u0, tg, sg, pb.options())
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        hi.run_cycle()
+        hi.monitor()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            it.append(a.elapsed_time(b))
+    return {"workload": f"{name}: {pb.name}", "value": relax_units(pb) / (ms * 1e-3),
+            "unit": UNIT, "ms_per_step": ms, "iteration_ms": statistics.median(it),
+            "point_updates_per_step": relax_units(pb)}
 
 
 def main():
