@@ -3255,10 +3255,16 @@ int fcf_dispatch(const mgp_phi &p, int64_t nc, Fn &&fn) {
     int run = run_length(p.nx, nc > 1 ? nc : 2);
     // WENO5 fields above 2048 cells (one CTA per SM with four shared arrays):
     // runs of 16 cells with the RK base in global memory, two CTAs per SM
-    // (Field U0G).  MGP_FCF_U0G=0 keeps the runs of 8.
-    if (p.weno_k == 2 && p.nx > 2048 && p.nx % 16 == 0) {
+    // (Field U0G).  MGP_FCF_U0G=0 keeps the runs of 8; MGP_FCF_U0G=n > 1
+    // applies the variant from n cells on (it also gains on smaller meshes
+    // when every CTA slot is busy -- 2048 cells 0.856 -> 0.874, 512 cells
+    // 0.839 -> 0.878 of the FP64 peak -- but loses on config 2 itself, whose
+    // 1025 chains then occupy under half of the slots).
+    if (p.weno_k == 2 && p.nx % 16 == 0) {
         const char *e = getenv("MGP_FCF_U0G");
-        if (!(e && atoi(e) == 0)) run = 16;
+        const int v = e ? atoi(e) : 1;             // 0: off, 1: default, > 1: smallest mesh
+        const int64_t least = v > 1 ? v : 2049;
+        if (v != 0 && p.nx >= least) run = 16;
     }
     switch (p.weno_k) {
 #define MGP_FCF_K(KK)                                                   \
