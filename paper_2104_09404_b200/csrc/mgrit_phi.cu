@@ -1031,8 +1031,72 @@ struct Field {
         return (0.5 * (fl + fr)) - (half_alpha * (ur - ul));
     }
 
+    // First order (K = 0) on full runs, one CTA per field: the "interface
+    // states" are the cells themselves (left state of i+1/2 = omega c_i, right
+    // state = omega c_{i+1}, omega = raw/raw), so a thread keeps the P + 2
+    // states of its run and its two neighbours in registers and forms alpha's
+    // contribution, the P + 1 fluxes and the rhs from them -- no interface
+    // arrays, no flux pass, one barrier (alpha) instead of three.  Same
+    // operations on the same values as the staged path (bit-identical).
+    static constexpr bool kReg0 = (K == 0 && kRel && CS == 1);
+    __device__ __forceinline__ void rhs_first_order(const Consts &k, double *A) {
+        constexpr bool kCheck = (MODEL != MGP_MODEL_BURGERS);
+        double sv[PC + 2];     // states of cells i0 - 1 .. i0 + PC
+        unsigned long long m = 0;
+        if (i0 < ns) {
+#pragma unroll
+            for (int x = 0; x < PC + 2; ++x) {
+                const double c = u_rel(x - 1);
+                double v = k.k0_omega * (CW(0, 0, 0) * c);
+                if (kCheck && !is_finite(c)) v = __longlong_as_double(kNaNBits);
+                sv[x] = v;
+                if (MODEL == MGP_MODEL_BURGERS && x >= 1) {
+                    // interfaces i0 .. i0 + PC - 1: left states sv[1..PC],
+                    // right states sv[2..PC+1]; a non-finite cell of the
+                    // run makes the reference's alpha NaN
+                    m = umax64(m, abs_bits(v));
+                    if (x <= PC && !is_finite(c)) m = kNaNBits;
+                }
+            }
+        }
+        double half_alpha;
+        if (MODEL == MGP_MODEL_BURGERS) {
+            m = warp_umax64(m);
+            const int tid = threadIdx.x;
+            if ((tid & 31) == 0) s_red(tid >> 5) = m;
+            __syncthreads();
+            const int nw = (blockDim.x + 31) >> 5;
+            m = warp_umax64((tid & 31) < nw ? s_red(tid & 31) : 0ull);
+            half_alpha = 0.5 * __longlong_as_double((long long)m);
+        } else {
+            half_alpha = k.half_alpha_adv;
+            __syncthreads();   // every run has read its neighbours' cells before any commit
+        }
+        if (i0 < ns) {
+            double fm = lf(k, sv[0], sv[1], half_alpha);
+            double neg[PC];
+#pragma unroll
+            for (int p = 0; p < PC; ++p) {
+                const double f = lf(k, sv[p + 1], sv[p + 2], half_alpha);
+                neg[p] = -(f - fm);
+                fm = f;
+            }
+            if (k.dx_pow2) {
+#pragma unroll
+                for (int p = 0; p < PC; ++p) A[p] = neg[p] * k.inv_dx;
+            } else {
+#pragma unroll
+                for (int p = 0; p < PC; ++p) A[p] = neg[p] / k.dx;
+            }
+        }
+    }
+
     __device__ __forceinline__ void rhs(const Consts &k, double *A, double *u0r = nullptr,
                                         int sg = 0) {
+        if (kReg0 && ns % PC == 0) {   // uniform over the CTA
+            rhs_first_order(k, A);
+            return;
+        }
         trace(1);
         unsigned long long m = reconstruct(k);
         trace(2);
