@@ -195,11 +195,13 @@ constexpr int kModelBurgersRoe = 8;
 // B200 (profiles/r02_fcf_unroll.txt; runs of 16: blocks of 4): C3 16.3 -> 17.8 G point-updates/s --
 // the 8-window block spilled 824 bytes at 128 registers, the 4-window block
 // none inside the loop, and its static schedule has 19 % fewer stall cycles
-// per window; C2 (runs of 4) 14.2 -> 14.6 G.  MGP_CENTRED_UNROLL overrides.
+// per window; C2 (runs of 4) 14.2 -> 14.6 G.  WENO3 windows are small enough
+// to unroll the whole run without spilling (+ 3-4 %, profiles/r02_order_probe.txt).
+// MGP_CENTRED_UNROLL overrides.
 #ifdef MGP_CENTRED_UNROLL
 #define MGP_CU(pc) MGP_CENTRED_UNROLL
 #else
-#define MGP_CU(pc) ((pc) >= 8 ? 4 : ((pc) >= 4 ? (pc) / 2 : (pc)))
+#define MGP_CU(pc) (K <= 1 ? (pc) : ((pc) >= 8 ? 4 : ((pc) >= 4 ? (pc) / 2 : (pc))))
 #endif
 #define MGP_PRAGMA(x) _Pragma(#x)
 #define MGP_UNROLL_(n) MGP_PRAGMA(unroll n)
