@@ -505,7 +505,8 @@ __device__ __forceinline__ void ll_send(unsigned long long *w, double v, unsigne
                  "l"(t | (bits & 0xffffffffull)), "l"(t | (bits >> 32))
                  : "memory");
 }
-__device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned tag) {
+__device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned tag,
+                                          unsigned long long *fail) {
     unsigned long long lo, hi;
     int spins = 0;
     do {
@@ -513,6 +514,9 @@ __device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned 
                      : "memory");
     } while (((unsigned)(lo >> 32) != tag || (unsigned)(hi >> 32) != tag) &&
              ++spins < kLLSpinLimit);
+    // a peer that never answered: the result is void; the launch that follows
+    // on this stream reports it (launch_t)
+    if (spins >= kLLSpinLimit) *fail = 1ull;
     return __longlong_as_double((long long)((hi << 32) | (lo & 0xffffffffull)));
 }
 
@@ -552,6 +556,7 @@ struct Field {
     // LL: the CS CTAs exchange through the global mailbox `mbox` (this
     // group's region) instead of distributed shared memory
     unsigned long long *mbox;
+    unsigned long long *ll_fail;   // set when a poll gave up (word after the mailbox)
     unsigned eA, eB, eC;      // tags of the last alpha / halo / partial-sum exchange
     bool halo_pending;        // halo cells were sent since the last sync()
     __device__ __forceinline__ unsigned long long *box(int par, int cta, int off) const {
@@ -636,9 +641,9 @@ struct Field {
             if (tid < 2 * H) {
                 const int par = eB & 1;
                 if (tid < H)
-                    s_u(sk(ns + H + tid)) = ll_recv(box(par, q, kLLFromRight + 2 * tid), eB);
+                    s_u(sk(ns + H + tid)) = ll_recv(box(par, q, kLLFromRight + 2 * tid), eB, ll_fail);
                 else
-                    s_u(sk(tid - H)) = ll_recv(box(par, q, kLLFromLeft + 2 * (tid - H)), eB);
+                    s_u(sk(tid - H)) = ll_recv(box(par, q, kLLFromLeft + 2 * (tid - H)), eB, ll_fail);
             }
             halo_pending = false;
         }
@@ -648,13 +653,13 @@ struct Field {
             const int tid = threadIdx.x, lane = tid & 31;
             const int par = eB & 1;
             if (tid < 32) {            // cells [-H, 0) = the left neighbour's last H cells
-                if (lane < H) s_u(sk(lane)) = ll_recv(box(par, q, kLLFromLeft + 2 * lane), eB);
+                if (lane < H) s_u(sk(lane)) = ll_recv(box(par, q, kLLFromLeft + 2 * lane), eB, ll_fail);
                 __syncwarp();
             }
             if (tid >> 5 == (ns / PC - 1) >> 5) {   // warp of the slab's last run
                 // cells [ns, ns + H) = the right neighbour's first H cells
                 if (lane < H)
-                    s_u(sk(ns + H + lane)) = ll_recv(box(par, q, kLLFromRight + 2 * lane), eB);
+                    s_u(sk(ns + H + lane)) = ll_recv(box(par, q, kLLFromRight + 2 * lane), eB, ll_fail);
                 __syncwarp();
             }
             halo_pending = false;
@@ -1129,11 +1134,11 @@ struct Field {
                     unsigned long long v = 0;
                     if (tid < CS)
                         v = (unsigned long long)__double_as_longlong(
-                            ll_recv(box(par, tid, kLLAlpha), eA));
+                            ll_recv(box(par, tid, kLLAlpha), eA, ll_fail));
                     v = warp_umax64(v);
                     if (tid == 0) s_cmax(0) = v;
                     if (tid < 3) {
-                        const double sv = ll_recv(box(par, q, kLLStates + 2 * tid), eA);
+                        const double sv = ll_recv(box(par, q, kLLStates + 2 * tid), eA, ll_fail);
                         if (tid < 2) s_edge(tid) = sv;
                         else s_L(0) = sv;
                     }
@@ -1596,7 +1601,7 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                     if (q == 0) {
                         double tt = 0.0;
                         for (int j = 0; j < CS; ++j)
-                            tt = tt + ll_recv(f.box(0, j, kLLPsum + 2 * tid), e);
+                            tt = tt + ll_recv(f.box(0, j, kLLPsum + 2 * tid), e, f.ll_fail);
                         a.partials[3 * b + tid] = tt;
                     }
                 } else {
@@ -1610,7 +1615,7 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                     __syncwarp();   // rank 0's three readers are done
                     if (tid == 0) {
                         if (q == 0) ll_send(f.box(0, 0, kLLAck), 0.0, f.eC);
-                        else (void)ll_recv(f.box(0, 0, kLLAck), f.eC);
+                        else (void)ll_recv(f.box(0, 0, kLLAck), f.eC, f.ll_fail);
                     }
                 }
             } else if (CS > 1) {
@@ -1639,6 +1644,7 @@ __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Con
     f.halo_pending = false;
     // LL: this group's region of the mailbox (zeroed by the launch)
     f.mbox = LL ? mbox + (size_t)(blockIdx.x / CS) * 2 * CS * kLLWords : nullptr;
+    f.ll_fail = LL ? mbox + (size_t)(gridDim.x / CS) * 2 * CS * kLLWords : nullptr;
     const int nx = (int)a.phi.nx;
     const int ns = nx / CS;            // cells of this CTA's slab
     const int q = (CS == 1) ? 0 : (int)(blockIdx.x % CS);
@@ -2887,6 +2893,27 @@ void *device_scratch(int kind, size_t bytes, cudaStream_t st, bool zero) {
     return bx->p;
 }
 
+// Pinned host word per (device, stream) that receives the LL give-up flag of
+// the last LL launch on that stream.
+unsigned long long *ll_fail_flag(cudaStream_t st) {
+    struct Flag {
+        int dev;
+        cudaStream_t st;
+        unsigned long long *p;
+    };
+    static std::vector<Flag> flags;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    for (auto &f : flags)
+        if (f.dev == dev && f.st == st) return f.p;
+    unsigned long long *p = nullptr;
+    if (cudaHostAlloc(&p, sizeof(unsigned long long), cudaHostAllocDefault) != cudaSuccess)
+        return nullptr;
+    *p = 0;
+    flags.push_back(Flag{dev, st, p});
+    return p;
+}
+
 template <int K, int REG, int MODEL, int P, int REGS, int CS, bool LL = false>
 int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     const int64_t ns = a.phi.nx / CS;
@@ -2921,8 +2948,17 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     } else if (LL) {
         // groups of CS co-resident CTAs (cooperative launch: all resident or
         // the launch fails), as many groups as fit the device
-        mbox = static_cast<unsigned long long *>(device_scratch(
-            0, (size_t)grid * 2 * CS * kLLWords * sizeof(unsigned long long), st, true));
+        // the previous LL launch on this stream gave up on a peer (its result is
+        // void): surface it now -- the flag travels back without a host wait
+        unsigned long long *fail_host = ll_fail_flag(st);
+        if (!fail_host) return MGP_ECUDA;
+        if (*fail_host) {
+            *fail_host = 0;
+            return MGP_ECUDA;
+        }
+        const size_t words = (size_t)grid * 2 * CS * kLLWords;
+        mbox = static_cast<unsigned long long *>(
+            device_scratch(0, (words + 1) * sizeof(unsigned long long), st, true));
         if (!mbox) return MGP_ECUDA;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid * CS));
@@ -2935,6 +2971,8 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox, u0_rows) != cudaSuccess) return MGP_ECUDA;
+        cudaMemcpyAsync(fail_host, mbox + words, sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost, st);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(grid * CS));
