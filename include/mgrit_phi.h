@@ -144,7 +144,9 @@ typedef struct mgp_phi {
  *                        tail_out2[b*to2_s] = guess == LAST_STEP
  *                                             ? phi + gf : aux2[b*aux2_s]
  *     MGP_TAIL_RESID:    r = (gf + Phi(x)) - aux[b*aux_s];
- *                        partials[3b+0] = sum over cells of r*r
+ *                        partials[3b+0] = sum over cells of r*r;
+ *                        if tail_out: tail_out[b*to_s] = gf + Phi(x)  (the value
+ *                        the next C-relaxation of the chunk computes)
  *                        (last chunk also accounts aux row in err/nonfinite
  *                         against ref[(b+1)*ref_cs] when ref_last_next != 0)
  *   partials (if non-NULL): [3b+0] residual^2, [3b+1] error^2 (ref non-NULL),

@@ -1547,11 +1547,15 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
                 const double *tgt = a.aux + b * a.aux_s;
                 const bool last = (b == a.n_chunks - 1) && a.ref_last_next;
                 const double *rn = (last && a.ref) ? a.ref + (b + 1) * a.ref_cs : nullptr;
+                // optional: keep g + Phi(x), which is the value the next
+                // C-relaxation of this chunk computes (mgrit.py:182-191)
+                double *keep = a.tail_out ? a.tail_out + b * a.to_s : nullptr;
                 for (int t = tid; t < ns; t += nt) {
                     const int c = c0 + t;
                     const double y = res(t);
                     const double pred =
                         (a.tail_g_mode == MGP_G_NONE) ? y : g_value(a.tail_g_mode, tg, c) + y;
+                    if (keep) keep[c] = pred;
                     const double u = tgt[c];
                     const double r = pred - u;
                     acc_r = acc_r + r * r;

@@ -95,6 +95,8 @@ def emulate_sweep(phi, *, n_chunks, start, start_stride, n_steps, g_mode, g, g_c
                 tgt = _rows(aux, aux_s, n, nx).numpy()
                 pred = y if tail_g_mode == 0 else (tg if tail_g_mode == 2 else 0.0) + y
                 acc_r[:] = ((pred - tgt) ** 2).sum(axis=1)
+                if tail_out is not None:     # the kept g + Phi(x) (mgp_sweep, MGP_TAIL_RESID)
+                    _rows(tail_out, to_s, n, nx).copy_(torch.from_numpy(np.ascontiguousarray(pred)))
                 if ref_last_next:
                     last = tgt[n - 1]
                     if ref is not None:

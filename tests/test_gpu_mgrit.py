@@ -251,3 +251,33 @@ def test_relax_to_host_graph_replay():
         g.load_c_points(c_host)
         g.relax(0)
         assert torch.equal(out, g.fine_values().cpu())
+
+
+def test_residual_row_feeds_the_next_c_relaxation():
+    """From the second iteration on the finest level's C-relaxation is a
+    buffer swap: the residual row before it kept Phi^m(C_j) + 0.0.  Same
+    record and trajectory, bit for bit, with fewer launches."""
+    pb = P.Problem(name="reuse", n_x=128, n_t=512, cfl=0.05, n_modes=4, n_levels=3, m=4,
+                   relaxation="fcf", max_iters=4)
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    out = {}
+    for reuse in (True, False):
+        P.MgritHierarchy.reuse_residual_for_relaxation = reuse
+        try:
+            n0 = P._lib.launch_count()
+            traj, rec = P.mgrit_solve(pb.steppers(tg), u0, tg, pb.space_grid(), pb.options())
+            out[reuse] = (traj.values, rec.residuals, P._lib.launch_count() - n0)
+        finally:
+            P.MgritHierarchy.reuse_residual_for_relaxation = True
+    assert np.array_equal(out[True][0], out[False][0])
+    assert np.array_equal(out[True][1], out[False][1])
+    assert out[True][2] == out[False][2] - 3      # iterations 2-4: one launch less each
+    # and against the oracle restatement
+    ost = [oracle.OracleStepper(k=2, rk_order=3, dt=tg.dt * 4 ** l, dx=1.0 / 128)
+           for l in range(3)]
+    otraj, orec = mgrit_oracle.mgrit_solve(
+        ost, u0, pb.n_t, tg.dt, mgrit_oracle.Options(n_levels=3, m=4, relaxation="fcf",
+                                                     max_iters=4))
+    assert np.array_equal(out[True][0], otraj)
+    np.testing.assert_allclose(out[True][1], orec.residuals, rtol=1e-10)
