@@ -1637,13 +1637,10 @@ __device__ __forceinline__ void sweep_body(const mgp_sweep_args &a, const Consts
 
 template <int K, int REG, int MODEL, int P, int REGS, int CS, bool LL = false>
 __global__ void __maxnreg__(REGS) sweep_kernel(const mgp_sweep_args a, const Consts k,
-                                               unsigned long long *mbox, double *u0_rows) {
-    // runs of 16 cells: the RK base in a global row per CTA (Field U0G), so
-    // that two CTAs of a 4096-cell field or slab share an SM
-    constexpr bool kU0G = (P == 16);
-    using F = Field<K, REG, MODEL, P, CS, LL, kU0G>;
+                                               unsigned long long *mbox) {
+    using F = Field<K, REG, MODEL, P, CS, LL>;
     F f;
-    f.u0g = kU0G ? u0_rows + (size_t)blockIdx.x * (size_t)blockDim.x * (P > 0 ? P : 1) : nullptr;
+    f.u0g = nullptr;
     f.eA = f.eB = f.eC = 0;
     f.halo_pending = false;
     // LL: this group's region of the mailbox (zeroed by the launch)
@@ -2863,8 +2860,7 @@ size_t smem_bytes(int64_t ns, int k, int cs, int p) {
 
 // Library-owned device scratch, one allocation per (kind, device, stream),
 // grown on demand: kind 0 = the LL mailbox (Field, LL mode; zeroed by every
-// launch that uses it, tags restart at 1), kind 1 = the RK-base rows of the
-// runs-of-16 sweep kernels (Field U0G; no initialisation needed).
+// launch that uses it, tags restart at 1).
 void *device_scratch(int kind, size_t bytes, cudaStream_t st, bool zero) {
     struct Box {
         int kind, dev;
@@ -2930,9 +2926,8 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
     if (grid > ((int64_t)1 << 30) / CS) grid = ((int64_t)1 << 30) / CS;
     const Consts k = make_consts(a.phi);
     unsigned long long *mbox = nullptr;
-    double *u0_rows = nullptr;
     int dev = 0, nsm = 0, per = 0;
-    if (P == 16 || LL) {
+    if (LL) {
         if (cudaGetDevice(&dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, sm) != cudaSuccess)
@@ -2942,13 +2937,8 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         if (groups < 1) return MGP_ECUDA;
         if (grid > groups) grid = groups;
     }
-    if (P == 16) {
-        u0_rows = static_cast<double *>(
-            device_scratch(1, (size_t)grid * CS * nt * 16 * sizeof(double), st, false));
-        if (!u0_rows) return MGP_ECUDA;
-    }
     if (CS == 1) {
-        kern<<<(unsigned)grid, nt, sm, st>>>(a, k, mbox, u0_rows);
+        kern<<<(unsigned)grid, nt, sm, st>>>(a, k, mbox);
     } else if (LL) {
         // groups of CS co-resident CTAs (cooperative launch: all resident or
         // the launch fails), as many groups as fit the device
@@ -2974,7 +2964,7 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox, u0_rows) != cudaSuccess) return MGP_ECUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
         cudaMemcpyAsync(fail_host, mbox + words, sizeof(unsigned long long),
                         cudaMemcpyDeviceToHost, st);
     } else {
@@ -2990,7 +2980,7 @@ int launch_t(const mgp_sweep_args &a, cudaStream_t st) {
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox, u0_rows) != cudaSuccess) return MGP_ECUDA;
+        if (cudaLaunchKernelEx(&cfg, kern, a, k, mbox) != cudaSuccess) return MGP_ECUDA;
     }
     ++g_launches;
     return cudaPeekAtLastError() == cudaSuccess ? MGP_OK : MGP_ECUDA;
