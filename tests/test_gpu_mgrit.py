@@ -192,9 +192,11 @@ def test_large_mesh_mgrit_on_clusters():
     np.testing.assert_allclose(rec.errors, orec.errors, rtol=1e-10)
 
 
-@pytest.mark.parametrize("relaxation,pieces", [("fcf", 8), ("fcf", 1), ("f", 3), ("fcf", 1000)])
-def test_relax_to_host_equals_relax_then_fine_values(relaxation, pieces):
-    pb = P.Problem(name="io", n_x=64, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4,
+@pytest.mark.parametrize("relaxation,pieces,n_x", [
+    ("fcf", 8, 64), ("fcf", 1, 64), ("f", 3, 64), ("fcf", 1000, 64),
+    ("fcf", 0, 2064), ("fcf", 3, 2064)])    # runs of 16 (RK base in global): zero-copy / pieces
+def test_relax_to_host_equals_relax_then_fine_values(relaxation, pieces, n_x):
+    pb = P.Problem(name="io", n_x=n_x, n_t=256, cfl=0.2, n_modes=3, n_levels=2, m=4,
                    relaxation=relaxation)
     u0 = pb.initial_state()
     tg = pb.time_grid(u0)
