@@ -41,7 +41,8 @@ from ._lib import (G_ARRAY, G_ZERO, GUESS_INJECTION, GUESS_LAST_STEP, SUM_SEQ,
                    TAIL_PHI, TAIL_RESID, TAIL_RESTRICT)
 from .errors import ConfigError, DimensionError
 from .grid import SpatialGrid, TemporalGrid, Trajectory
-from .mgrit import ConvergenceRecord, Monitor, MgritOptions, _check_stepper, _ref_norm_sq
+from .mgrit import (ConvergenceRecord, Monitor, MgritHierarchy, MgritOptions, _check_stepper,
+                    _ref_norm_sq)
 
 
 def partition(n_steps: int, m: int, n_levels: int, world: int):
@@ -164,6 +165,7 @@ class DistMgritHierarchy:
             dev.sweep(phi, n_chunks=1, start=cd[0], start_stride=0, n_steps=m - 1,
                       g_mode=G_ZERO, store=out[1], st_ss=nx, what="relax_fine_values/f0")
         self._cur = self._fsrc = d
+        self._crelax_done = None
         self._pristine = False
         return out
 
@@ -198,6 +200,7 @@ class DistMgritHierarchy:
             dev.sweep(phi, n_chunks=1, start=cd[0], start_stride=0, n_steps=m - 1,
                       g_mode=G_ZERO, store=th[1], st_ss=nx, what="relax_to_host/f0")
         self._cur = self._fsrc = d
+        self._crelax_done = None
         self._pristine = False
 
     def _other(self, i):
@@ -289,9 +292,21 @@ class DistMgritHierarchy:
                 dev.sweep(phi, n_chunks=n0, start=self._u0, start_stride=0, tail=TAIL_PHI,
                           tail_regime=regime, tail_g_mode=G_ZERO, tail_out=dst[1], to_s=nx,
                           what="c_relax")
+            elif (getattr(self, "_crelax_done", None) is not None
+                  and self._crelax_done == self._fsrc == self._cur):
+                # the residual row kept Phi^m(C_j) + 0.0 of every local
+                # interval in the other buffer (monitor): this C-relaxation is
+                # a buffer swap; the boundary exchange follows as always
+                src = self._cur
+                d = 1 - src
+                self._c[d][0].copy_(self._c[src][0])
+                self._cur = d
+                self._crelax_done = None
+                dst = self._c[d]
             else:
                 src = self._fsrc
                 ws = self._fcf_workspace()
+                self._crelax_done = None
                 if self._cur == src:
                     d = self._other(src)
                     if ws is None:
@@ -430,6 +445,7 @@ class DistMgritHierarchy:
             src = self._scatter_rows(self._u[l + 1] if self.r == 0 else None, nc + 1, nc)
         if l == 0:
             self._c[self._cur].copy_(src)
+            self._crelax_done = None
             self._pristine = False
         else:
             self._u[l][::m].copy_(src)
@@ -494,11 +510,17 @@ class DistMgritHierarchy:
             return Monitor(math.sqrt(nt * r2), e2, int(nf))
         if self._fsrc == self._cur and self._regime(0) == SUM_SEQ:
             c = self._c[self._cur]
+            # keep 0.0 + Phi^m(C_j) for the next C-relaxation (MgritHierarchy.monitor)
+            keep = None
+            if MgritHierarchy.reuse_residual_for_relaxation and self.options.relaxation == "fcf":
+                keep = self._c[self._other(self._cur)]
             dev.sweep(self._phi(0, self._regime(0)), n_chunks=n0, start=c, start_stride=nx,
                       n_steps=m - 1, g_mode=G_ZERO, ref=ref, ref_cs=m * nx, ref_ss=nx,
                       ref_last_next=last, count_nonfinite=1, tail=TAIL_RESID,
                       tail_regime=resid_regime, tail_g_mode=G_ZERO, aux=c[1], aux_s=nx,
-                      partials=self._partials, what="monitor")
+                      partials=self._partials,
+                      tail_out=None if keep is None else keep[1], to_s=nx, what="monitor")
+            self._crelax_done = None if keep is None else self._cur
             r2, e2, nf = self._reduced(n0)
             return Monitor(math.sqrt(r2), e2, int(nf))
         traj = self._local_values().reshape(-1, nx)       # n0*m + 1 rows
@@ -559,6 +581,7 @@ class DistMgritHierarchy:
         c.copy_(src.reshape(c.shape), non_blocking=True)
         self._fsrc = self._cur
         self._pristine = False
+        self._crelax_done = None
 
 
 def mgrit_solve_distributed(steppers, initial_state, time_grid, space_grid,
