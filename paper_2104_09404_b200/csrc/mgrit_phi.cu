@@ -531,14 +531,21 @@ __device__ __forceinline__ double ll_recv(const unsigned long long *w, unsigned 
 // alpha is reduced over the cluster.
 // 256-bit global accesses (sm_100): a thread's slice of its CTA's RK-base row
 __device__ __forceinline__ void ldg_cg4(const double *p, double *v) {
-    asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate.L2::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
                  : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                  : "l"(p)
                  : "memory");
 }
 __device__ __forceinline__ void stg_cg4(double *p, const double *v) {
-    asm volatile("st.global.cg.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]),
+    asm volatile("st.global.L1::no_allocate.L2::evict_last.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]),
                  "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
+__device__ __forceinline__ void stg_stream4(double *p, const double *v) {
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(
+                     p),
+                 "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
                  : "memory");
 }
 
@@ -2180,11 +2187,26 @@ __global__ void __maxnreg__(REGS) fcf_kernel(const mgp_fcf_args a, const Consts 
         for (int st = s0; st <= s1; ++st) {
             f.sync();
             if (dst || dst2 || dst3) {
-                for (int c = tid; c < ns; c += nt) {
-                    const double v = f.cell(c);
-                    if (dst) dst[c] = v;
-                    if (dst2) dst2[c] = v;
-                    if (dst3) __stcg(dst3 + c, v);
+                const bool wide = !dst3 && ns % 4 == 0 &&
+                                  ((reinterpret_cast<uintptr_t>(dst) |
+                                    reinterpret_cast<uintptr_t>(dst2)) & 31) == 0;
+                if (wide) {
+                    // streaming output: 256-bit stores with L2 evict-first
+                    // priority (written once, never read by this launch)
+                    for (int c = 4 * tid; c < ns; c += 4 * nt) {
+                        double v[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) v[i] = f.cell(c + i);
+                        if (dst) stg_stream4(dst + c, v);
+                        if (dst2) stg_stream4(dst2 + c, v);
+                    }
+                } else {
+                    for (int c = tid; c < ns; c += nt) {
+                        const double v = f.cell(c);
+                        if (dst) dst[c] = v;
+                        if (dst2) dst2[c] = v;
+                        if (dst3) __stcg(dst3 + c, v);
+                    }
                 }
             }
             if (st == s1) break;
