@@ -32,7 +32,7 @@ STATUS_NONPOSITIVE_DEPTH = 1
 STATUS_NONPOSITIVE_DENSITY = 2
 STATUS_NONPOSITIVE_PRESSURE = 4
 STATUS_ROE_NONHYPERBOLIC = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -3606,7 +3606,7 @@ int mgp_sum_partials(const double *partials, int64_t n, int32_t width, double *o
 
 int64_t mgp_max_nx(int32_t weno_k, int32_t model) { return max_nx_for(weno_k, model); }
 
-int32_t mgp_abi_version(void) { return 5; }
+int32_t mgp_abi_version(void) { return 6; }   // 6: MGP_TAIL_RESID honours tail_out
 
 int mgp_weno_tables(int32_t k, double *cw16, double *d4, double *sm64) {
     if (k < 0 || k > 3 || !cw16 || !d4 || !sm64) return MGP_EINVAL;
