@@ -180,3 +180,46 @@ def test_sw_physical_state_divergence(name):
     _, rec2 = P.mgrit_solve(st2, u0, tg2, sg, P.MgritOptions(
         n_levels=spec["n_levels"], m=spec["m"], relaxation=spec["relaxation"], max_iters=2))
     assert not rec2.diverged
+
+
+def test_c5_full_size_first_iteration():
+    """BASELINE config 5 at its own size (N_x = 65536, N_t = 262144, m = 16,
+    35.5 GB of device arrays): residual row 0 against the oracle (every node
+    holds u0, so r = Phi(u0) - u0 at each of the N_t nodes: one oracle
+    propagator application), one V-cycle on the LL groups, the outcome of
+    iteration 1 equal to the scaled fixtures' (divergence: the config's CFL is
+    far above what its 16x coarsening tolerates), and the same iterate, bit
+    for bit, on the thread-block-cluster path."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~36 GB of device memory per hierarchy")
+    pb = P.BASELINE_CONFIGS["c5"]
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    p = pb.phi_params(0)
+    phi_u0 = oracle.phi_apply(
+        oracle.make_params(k=p["k"], rk_order=p["rk_order"], dt=p["dt"], dx=p["dx"],
+                           eps=p["eps"], regime=oracle.SUM_SEQ), u0[None])[0]
+    want_row0 = float(np.sqrt(pb.n_t * np.sum((phi_u0 - u0) ** 2)))
+    out = {}
+    for ll in ("1", "0"):
+        os.environ["MGP_LL"] = ll
+        try:
+            h_out = []
+            _, rec = P.mgrit_solve(pb.steppers(tg), u0, tg, pb.space_grid(),
+                                   P.MgritOptions(n_levels=pb.n_levels, m=pb.m,
+                                                  relaxation="fcf", max_iters=1),
+                                   return_trajectory=False, hierarchy_out=h_out)
+            c = h_out[0]._c[h_out[0]._cur]
+            out[ll] = (rec, canonical_hash(c[:2048].cpu().numpy()),
+                       canonical_hash(c[-2048:].cpu().numpy()))
+            del h_out, c
+            torch.cuda.empty_cache()
+        finally:
+            os.environ.pop("MGP_LL", None)
+    rec = out["1"][0]
+    np.testing.assert_allclose(rec.residuals[0], want_row0, rtol=RTOL)
+    assert rec.diverged_at == 1 and not np.isfinite(rec.residuals[1])
+    assert out["0"][0].diverged_at == 1
+    assert out["0"][0].residuals[0] == rec.residuals[0]
+    assert out["1"][1:] == out["0"][1:]
