@@ -223,3 +223,30 @@ def test_c5_full_size_first_iteration():
     assert out["0"][0].diverged_at == 1
     assert out["0"][0].residuals[0] == rec.residuals[0]
     assert out["1"][1:] == out["0"][1:]
+
+
+def test_c3_full_size_relaxation_kernels_agree():
+    """The two fused-FCF kernels -- runs of 16 cells with the RK base in global
+    memory (two CTAs per SM, the default above 2048 cells) and runs of 8 --
+    give the same config-3 relaxation, bit for bit (2.1 GB compared on the
+    device); the oracle anchors the default above."""
+    pb = P.BASELINE_CONFIGS["c3"]
+    u0 = pb.initial_state()
+    tg = pb.time_grid(u0)
+    steppers = pb.steppers(tg)
+    nc = pb.n_t // pb.m
+    c = np.stack([np.roll(u0[0], 3 * j % pb.n_x) for j in range(nc + 1)])
+    c = c + 1e-3 * np.random.default_rng(7).standard_normal(c.shape)
+    outs = []
+    for flag in ("1", "0"):
+        os.environ["MGP_FCF_U0G"] = flag
+        try:
+            h = P.MgritHierarchy(steppers, u0, tg, pb.space_grid(), pb.options())
+            h.load_c_points(c)
+            outs.append((h.relax_fine_values(), h._c[h._cur].clone()))
+            del h
+        finally:
+            os.environ.pop("MGP_FCF_U0G", None)
+    assert torch.isfinite(outs[0][0]).all()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
