@@ -961,7 +961,11 @@ struct Field {
                 if (!is_finite(win[K])) m = kNaNBits;
             }
         }
-        if (!ok) m = reconstruct_run_exact(k, n, false);
+        // A non-finite centre cell already made this run's alpha bits NaN:
+        // the field's alpha is NaN and every flux NaN whatever the states
+        // are, so the exact pass has nothing to repair (diverged iterates
+        // are mostly such fields).
+        if (!ok && !(burg && m == kNaNBits)) m = reconstruct_run_exact(k, n, false);
         return m;
     }
 
